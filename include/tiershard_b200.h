@@ -1,0 +1,194 @@
+/*
+ * tiershard_b200.h — C-ABI of the B200 device path (libtiershard_b200.so).
+ *
+ * The reference (tiershard 0.1.0, /root/reference/proj) is a C++ library with
+ * no device code and no C-ABI.  Its hot path is the per-iteration routing loop
+ * inside simulate() (/root/reference/proj/src/simulator.cpp:215-257), which
+ * only COUNTS traffic; the lookup/update entry points the north star asks for
+ * (gather, exchange, dedup, optimizer) have no reference counterpart
+ * (SURVEY.md §8a rows a16-a20).  This header is the thin layer the host C++
+ * API (include/tiershard/ *.hpp) crosses to reach CUDA; INTEGRATION.md shows
+ * how a reference user binds it (C++ relink, or the ctypes stub).
+ *
+ * Conventions
+ *   - plain C types only; no CUDA, NCCL or torch types cross this boundary
+ *     (streams are exposed as opaque void*);
+ *   - every entry point returns a ts_status; on failure ts_last_error()
+ *     returns the message for the calling thread.  The C++ shim rethrows
+ *     TS_ERR_CONFIG / TS_ERR_VALIDATION / TS_ERR_INTERNAL as
+ *     tiershard::ConfigError / ValidationError / Error with the same text,
+ *     and every device/NCCL failure as tiershard::Error;
+ *   - "rows" are canonical row indices (the u32 index space of
+ *     RowDistribution's canonical order, distribution.hpp:26-30);
+ *   - `tier_dest[i]` is the per-canonical-row placement byte emitted by the
+ *     host planner: the RW owner GPU (h % U, simulator.cpp:103-104) for
+ *     i >= flex_cut, the Flex slot (h % W, simulator.cpp:99-101) for
+ *     dp_cut <= i < flex_cut, ignored for DP rows (i < dp_cut);
+ *   - a handle is not reentrant: one host thread drives one handle.
+ *   - there is no CPU fallback: without a CUDA device every call that needs
+ *     one returns TS_ERR_NO_DEVICE.
+ */
+#ifndef TIERSHARD_B200_H_
+#define TIERSHARD_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TS_ABI_VERSION 1
+
+typedef enum ts_status {
+  TS_OK = 0,
+  TS_ERR_CONFIG = 1,     /* -> tiershard::ConfigError     (error.hpp:18-21)  */
+  TS_ERR_VALIDATION = 2, /* -> tiershard::ValidationError (error.hpp:25-28)  */
+  TS_ERR_INTERNAL = 3,   /* -> tiershard::Error           (error.hpp:12-15)  */
+  TS_ERR_CUDA = 4,       /* CUDA runtime / launch failure -> tiershard::Error */
+  TS_ERR_NCCL = 5,       /* NCCL failure -> tiershard::Error                  */
+  TS_ERR_NO_DEVICE = 6   /* no usable sm_100 device -> tiershard::Error       */
+} ts_status;
+
+/* Counter block layout returned by the routing entry points: 7 vectors of
+ * U uint64 each, [counter][gpu], in this order.  The first six are the
+ * reference's GpuCounters (simulator.cpp:112-119), the seventh its distinct
+ * served-row count (simulator.cpp:250-255). */
+enum {
+  TS_CTR_SEND_GLOBAL = 0,
+  TS_CTR_RECV_GLOBAL = 1,
+  TS_CTR_SEND_INTRA = 2,
+  TS_CTR_RECV_INTRA = 3,
+  TS_CTR_DP_LOCAL = 4,
+  TS_CTR_SERVED = 5,
+  TS_CTR_DISTINCT = 6,
+  TS_NUM_COUNTERS = 7
+};
+
+enum { TS_OPT_SGD = 0, TS_OPT_ROWWISE_ADAGRAD = 1 };
+
+/* Thread-local message of the last failing call on this thread. */
+const char* ts_last_error(void);
+/* ABI version, build flags, CUDA/NCCL versions. */
+const char* ts_build_info(void);
+int ts_abi_version(void);
+/* Number of CUDA devices visible (0 when no driver/device). */
+ts_status ts_device_count(int* count);
+
+/* ------------------------------------------------------------------------
+ * Router: the reference's routing + traffic-accounting loop on one GPU for a
+ * LOGICAL cluster of U = N*W GPUs (every requester's samples of one
+ * iteration are routed in one launch).  Replaces the per-occurrence loop of
+ * simulate() (simulator.cpp:215-257); the host shim derives
+ * IterationMetrics from the counters with the reference formulas
+ * (simulator.cpp:259-331).
+ * ---------------------------------------------------------------------- */
+typedef struct ts_router ts_router;
+
+/* Uploads the remap table (tier from the cuts, tier_dest byte per row).
+ * Requires 1 <= U <= 256 and n_rows < 2^32. */
+ts_status ts_router_create(ts_router** out, int device, uint64_t n_rows,
+                           uint64_t dp_cut, uint64_t flex_cut,
+                           const uint8_t* tier_dest, uint32_t num_nodes,
+                           uint32_t gpus_per_node);
+
+/* One iteration: host CSR (sample_offsets has U*local_batch+1 entries,
+ * GPU-major), copied to HBM, routed, 7*U counters copied back to host. */
+ts_status ts_router_iteration(ts_router* r, uint32_t local_batch,
+                              const uint64_t* sample_offsets,
+                              const uint32_t* rows, uint64_t occurrences,
+                              uint64_t* counters);
+
+/* Same, with device-resident inputs (no copies); counters to host. */
+ts_status ts_router_iteration_device(ts_router* r, const uint64_t* d_requester_begin,
+                                     const uint32_t* d_rows, uint64_t occurrences,
+                                     uint64_t* counters);
+
+ts_status ts_router_destroy(ts_router* r);
+
+/* ------------------------------------------------------------------------
+ * Sharded sequence-embedding table: lookup (forward) and update (backward)
+ * for one rank of a U = N*W GPU job.  Rank g stores, in one contiguous fp32
+ * [local_rows x dim] shard: the dp_cut DP rows, the Flex rows of slot g % W,
+ * and the RW rows it owns.  With U > 1 the ranks
+ * exchange ids/rows with NCCL (world communicator for RW, intra-node
+ * communicator g / W for Flex) and all-reduce DP (world) and Flex (cross
+ * communicator g % W) gradients.
+ * ---------------------------------------------------------------------- */
+typedef struct ts_table ts_table;
+
+typedef struct ts_table_config {
+  uint32_t num_nodes;      /* N */
+  uint32_t gpus_per_node;  /* W */
+  uint32_t rank;           /* g in [0, N*W) */
+  int32_t device;          /* CUDA ordinal */
+  uint32_t dim;            /* D: multiple of 32, <= 1024 */
+  uint64_t n_rows;         /* canonical rows (< 2^32) */
+  uint64_t dp_cut;
+  uint64_t flex_cut;
+  uint64_t weight_seed;    /* orc_init_weight contract, oracle/restate.h */
+  int32_t optimizer;       /* TS_OPT_* */
+  float lr;
+  float eps;               /* Adagrad epsilon */
+  uint64_t max_occurrences;      /* capacity: occurrences per step, this rank */
+  const void* nccl_unique_id;    /* 128-byte ncclUniqueId; NULL iff N*W == 1 */
+} ts_table_config;
+
+/* Collective over all U ranks when U > 1 (NCCL communicator creation). */
+ts_status ts_table_create(ts_table** out, const ts_table_config* cfg,
+                          const uint8_t* tier_dest);
+ts_status ts_table_destroy(ts_table* t);
+
+/* Rows of this rank's shard by tier. */
+ts_status ts_table_shard_rows(ts_table* t, uint64_t* dp_rows,
+                              uint64_t* flex_rows, uint64_t* rw_rows);
+
+/* The table's CUDA stream (cudaStream_t as void*). */
+ts_status ts_table_stream(ts_table* t, void** stream);
+
+/* Forward: d_rows are this rank's occurrences (device memory, canonical
+ * indices); writes the unpooled [occ x dim] fp32 embeddings to d_out. */
+ts_status ts_table_forward(ts_table* t, const uint32_t* d_rows, uint64_t occ,
+                           float* d_out);
+
+/* Backward + update for the last forward: d_grad is [occ x dim] (may alias
+ * that forward's d_out).  Dedup, segment-reduce, all-reduce of replicated
+ * tiers, fused optimizer. */
+ts_status ts_table_backward(ts_table* t, const float* d_grad);
+
+/* One synthetic training step: forward, loss = 0.5*sum(out^2) (device),
+ * backward with grad = out.  Device inputs; no host synchronisation. */
+ts_status ts_table_train_step(ts_table* t, const uint32_t* d_rows,
+                              uint64_t occ, float* d_out);
+
+/* End-to-end step through host memory: copies h_rows (pinned or pageable)
+ * to HBM, runs ts_table_train_step, and reads the loss back to *h_loss. */
+ts_status ts_table_train_step_host(ts_table* t, const uint32_t* h_rows,
+                                   uint64_t occ, double* h_loss);
+
+/* Loss of the last train step (synchronises the table stream). */
+ts_status ts_table_loss(ts_table* t, double* loss);
+
+/* This rank's counter contribution for the last forward/backward: for the
+ * requester side its own column, for the server side the occurrences and
+ * distinct rows it served (filled in by backward). 7*U host uint64. */
+ts_status ts_table_counters(ts_table* t, uint64_t* counters);
+
+/* Copies rows (canonical indices stored on this rank) and, for Adagrad,
+ * their state back to host.  ValidationError for rows not on this rank. */
+ts_status ts_table_read_rows(ts_table* t, const uint32_t* rows, uint64_t count,
+                             float* h_weights, float* h_state);
+
+ts_status ts_table_synchronize(ts_table* t);
+
+/* Per-phase device time accumulated since the last reset (CUDA events on the
+ * table stream), in ms: see ts_table_phase_name for the index meaning. */
+ts_status ts_table_enable_timing(ts_table* t, int enable);
+ts_status ts_table_phase_times(ts_table* t, double* ms, uint64_t* launches,
+                               int capacity, int* count);
+const char* ts_table_phase_name(int phase);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TIERSHARD_B200_H_ */

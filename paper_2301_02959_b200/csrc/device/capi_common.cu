@@ -1,0 +1,77 @@
+// C-ABI entry points shared by every handle: error reporting, build info,
+// device discovery (include/tiershard_b200.h).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <string>
+
+#include "common.cuh"
+
+namespace tsd {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+void use_device(int device) {
+  int count = 0;
+  const cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    fail(TS_ERR_NO_DEVICE, "no CUDA device available (the tiershard-b200 device path has no CPU "
+                           "fallback)");
+  }
+  if (device < 0 || device >= count) {
+    fail(TS_ERR_CONFIG, "CUDA device " + std::to_string(device) + " out of range (" +
+                            std::to_string(count) + " visible)");
+  }
+  TSD_CUDA(cudaSetDevice(device));
+  int major = 0;
+  TSD_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major != 10) {
+    fail(TS_ERR_NO_DEVICE, "device " + std::to_string(device) +
+                               " is not an sm_100 (Blackwell) part; this build targets sm_100a only");
+  }
+}
+
+int sm_count() {
+  int dev = 0, n = 0;
+  TSD_CUDA(cudaGetDevice(&dev));
+  TSD_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  return n;
+}
+
+}  // namespace tsd
+
+extern "C" {
+
+const char* ts_last_error(void) { return tsd::g_last_error.c_str(); }
+
+int ts_abi_version(void) { return TS_ABI_VERSION; }
+
+const char* ts_build_info(void) {
+  static const std::string info = [] {
+    int rt = 0;
+    cudaRuntimeGetVersion(&rt);
+    return std::string("tiershard-b200 abi=") + std::to_string(TS_ABI_VERSION) +
+           " arch=sm_100a cudart=" + std::to_string(rt) +
+           " nccl_headers=" + std::to_string(NCCL_VERSION_CODE);
+  }();
+  return info.c_str();
+}
+
+ts_status ts_device_count(int* count) {
+  return tsd::guarded([&] {
+    if (!count) tsd::fail(TS_ERR_CONFIG, "ts_device_count: null output");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    *count = n;
+  });
+}
+
+}  // extern "C"

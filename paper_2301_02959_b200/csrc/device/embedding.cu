@@ -1,0 +1,449 @@
+// Value-path kernels (embedding.cuh): unpooled gather, deterministic
+// segment-reduce with fused row-wise SGD / Adagrad, dense replica updates.
+//
+// Lane layout used everywhere a warp owns one embedding row: lane l holds the
+// VEC = dim/32 contiguous floats [l*VEC, (l+1)*VEC) — 128-bit accesses for
+// dim >= 128, 64-bit for dim = 64.  The Adagrad sum of squares is the
+// per-lane fma chain followed by the xor butterfly, exactly the order
+// oracle/restate.c replays, so single-GPU results are bit-identical.
+// Every floating-point op in the update is an explicit _rn intrinsic: no
+// contraction or fast-math can change a bit.
+#include "common.cuh"
+#include "embedding.cuh"
+#include "primitives.cuh"
+
+namespace tsd {
+namespace {
+
+constexpr int kThreads = 256;
+
+template <int VEC>
+__device__ __forceinline__ void load_lane(const float* p, float (&r)[VEC]) {
+  if constexpr (VEC % 4 == 0) {
+#pragma unroll
+    for (int j = 0; j < VEC / 4; ++j) {
+      const float4 t = *reinterpret_cast<const float4*>(p + 4 * j);
+      r[4 * j] = t.x;
+      r[4 * j + 1] = t.y;
+      r[4 * j + 2] = t.z;
+      r[4 * j + 3] = t.w;
+    }
+  } else if constexpr (VEC == 2) {
+    const float2 t = *reinterpret_cast<const float2*>(p);
+    r[0] = t.x;
+    r[1] = t.y;
+  } else {
+    r[0] = *p;
+  }
+}
+
+template <int VEC>
+__device__ __forceinline__ void load_lane_ro(const float* p, float (&r)[VEC]) {
+  if constexpr (VEC % 4 == 0) {
+#pragma unroll
+    for (int j = 0; j < VEC / 4; ++j) {
+      const float4 t = __ldg(reinterpret_cast<const float4*>(p + 4 * j));
+      r[4 * j] = t.x;
+      r[4 * j + 1] = t.y;
+      r[4 * j + 2] = t.z;
+      r[4 * j + 3] = t.w;
+    }
+  } else if constexpr (VEC == 2) {
+    const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+    r[0] = t.x;
+    r[1] = t.y;
+  } else {
+    r[0] = __ldg(p);
+  }
+}
+
+template <int VEC>
+__device__ __forceinline__ void store_lane(float* p, const float (&r)[VEC]) {
+  if constexpr (VEC % 4 == 0) {
+#pragma unroll
+    for (int j = 0; j < VEC / 4; ++j) {
+      *reinterpret_cast<float4*>(p + 4 * j) =
+          make_float4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+    }
+  } else if constexpr (VEC == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(r[0], r[1]);
+  } else {
+    *p = r[0];
+  }
+}
+
+// Canonical row -> local shard row of THIS rank, false if served remotely.
+__device__ __forceinline__ bool resolve_local(const RemapView& rv, uint32_t c, uint32_t* lid) {
+  if (rv.identity || c < rv.dp_cut) {
+    *lid = c;
+    return true;
+  }
+  const uint32_t d = __ldg(rv.dest + c);
+  const bool mine = c < rv.flex_cut ? d == rv.slot : d == rv.rank;
+  if (mine) *lid = __ldg(rv.local + c);
+  return mine;
+}
+
+template <int DIM, int UNROLL>
+__global__ void __launch_bounds__(kThreads)
+gather_local_kernel(const uint32_t* __restrict__ rows, uint64_t occ,
+                    const float* __restrict__ weights, float* __restrict__ out, RemapView rv,
+                    double* __restrict__ loss_partials) {
+  constexpr int VEC = DIM / 32;
+  __shared__ float s_sq[kThreads / 32];
+  const unsigned lane = threadIdx.x & 31u;
+  const uint64_t gwarp = (static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * kThreads) >> 5;
+  float sq = 0.0f;
+  for (uint64_t base = gwarp * UNROLL; base < occ; base += nwarps * UNROLL) {
+    uint32_t my_lid = 0;
+    bool my_ok = false;
+    if (lane < UNROLL && base + lane < occ) my_ok = resolve_local(rv, __ldg(rows + base + lane), &my_lid);
+    float r[UNROLL][VEC];
+    bool ok[UNROLL];
+#pragma unroll
+    for (int k = 0; k < UNROLL; ++k) {
+      const uint32_t lid = __shfl_sync(0xFFFFFFFFu, my_lid, k);
+      ok[k] = __shfl_sync(0xFFFFFFFFu, my_ok, k);
+      if (ok[k]) load_lane_ro<VEC>(weights + static_cast<uint64_t>(lid) * DIM + lane * VEC, r[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < UNROLL; ++k) {
+      if (ok[k]) {
+        store_lane<VEC>(out + (base + k) * DIM + lane * VEC, r[k]);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) sq = __fmaf_rn(r[k][j], r[k][j], sq);
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, m);
+  if (lane == 0) s_sq[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) acc += static_cast<double>(s_sq[w]);
+    loss_partials[blockIdx.x] = acc;
+  }
+}
+
+__global__ void loss_finalize_kernel(const double* __restrict__ partials, unsigned count,
+                                     double* __restrict__ loss) {
+  // one thread, fixed order: deterministic for a fixed grid
+  double acc = 0.0;
+  for (unsigned i = 0; i < count; ++i) acc += partials[i];
+  *loss = 0.5 * acc;
+}
+
+// ---------------------------------------------------------------------------
+// segment reduction + optimizer
+// ---------------------------------------------------------------------------
+
+template <int VEC>
+__device__ __forceinline__ const float* grad_row(const GradSource& gs, uint32_t v, uint32_t dim) {
+  return v < gs.n_local ? gs.local + static_cast<uint64_t>(v) * dim
+                        : gs.remote + static_cast<uint64_t>(v - gs.n_local) * dim;
+}
+
+// Finishes one reduced row: dense-range rows park their gradient, others get
+// the optimizer step.  All 32 lanes must call (Adagrad uses shuffles).
+template <int DIM>
+__device__ __forceinline__ void finish_row(uint32_t row, const float (&g)[DIM / 32],
+                                           float* __restrict__ weights, float* __restrict__ state,
+                                           const OptParams& opt, const DenseRange& d0,
+                                           const DenseRange& d1) {
+  constexpr int VEC = DIM / 32;
+  const unsigned lane = threadIdx.x & 31u;
+  if (row >= d0.lo && row < d0.hi) {
+    store_lane<VEC>(d0.grad + static_cast<uint64_t>(row - d0.lo) * DIM + lane * VEC, g);
+    return;
+  }
+  if (row >= d1.lo && row < d1.hi) {
+    store_lane<VEC>(d1.grad + static_cast<uint64_t>(row - d1.lo) * DIM + lane * VEC, g);
+    return;
+  }
+  float* wp = weights + static_cast<uint64_t>(row) * DIM + lane * VEC;
+  float w[VEC];
+  load_lane<VEC>(wp, w);
+  if (opt.optimizer == TS_OPT_SGD) {
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) w[j] = __fmaf_rn(-opt.lr, g[j], w[j]);
+  } else {
+    float q = 0.0f;
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) q = __fmaf_rn(g[j], g[j], q);
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) q = __fadd_rn(q, __shfl_xor_sync(0xFFFFFFFFu, q, m));
+    const float G = __fadd_rn(state[row], __fdiv_rn(q, static_cast<float>(DIM)));
+    __syncwarp();
+    if (lane == 0) state[row] = G;
+    const float denom = __fadd_rn(__fsqrt_rn(G), opt.eps);
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) w[j] = __fmaf_rn(-opt.lr, __fdiv_rn(g[j], denom), w[j]);
+  }
+  store_lane<VEC>(wp, w);
+}
+
+// acc = sum of grad rows vals[s..e) left to right (acc starts from entry s).
+template <int DIM>
+__device__ __forceinline__ void sum_entries(const uint32_t* __restrict__ vals, uint32_t s,
+                                            uint32_t e, const GradSource& gs,
+                                            float (&acc)[DIM / 32]) {
+  constexpr int VEC = DIM / 32;
+  constexpr int B = DIM <= 128 ? 8 : 4;  // rows in flight per warp
+  const unsigned lane = threadIdx.x & 31u;
+  load_lane<VEC>(grad_row<VEC>(gs, __ldg(vals + s), DIM) + lane * VEC, acc);
+  uint32_t k = s + 1;
+  for (; k + B <= e; k += B) {
+    const uint32_t my_v = lane < B ? __ldg(vals + k + lane) : 0u;
+    float r[B][VEC];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const uint32_t v = __shfl_sync(0xFFFFFFFFu, my_v, b);
+      load_lane<VEC>(grad_row<VEC>(gs, v, DIM) + lane * VEC, r[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) acc[j] = __fadd_rn(acc[j], r[b][j]);
+    }
+  }
+  for (; k < e; ++k) {
+    float r[VEC];
+    load_lane<VEC>(grad_row<VEC>(gs, __ldg(vals + k), DIM) + lane * VEC, r);
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) acc[j] = __fadd_rn(acc[j], r[j]);
+  }
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(kThreads)
+seg_short_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                 const uint32_t* __restrict__ starts, const uint32_t* __restrict__ d_nseg,
+                 GradSource gs, float* __restrict__ weights, float* __restrict__ state,
+                 OptParams opt, DenseRange d0, DenseRange d1, uint32_t* __restrict__ long_list,
+                 uint32_t* __restrict__ long_count) {
+  const unsigned lane = threadIdx.x & 31u;
+  const uint32_t nseg = *d_nseg;
+  const uint32_t gwarp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
+  for (uint32_t j = gwarp; j < nseg; j += nwarps) {
+    const uint32_t s = __ldg(starts + j), e = __ldg(starts + j + 1);
+    if (e - s > kPiece) {
+      if (lane == 0) long_list[atomicAdd(long_count, 1u)] = j;
+      continue;
+    }
+    float acc[DIM / 32];
+    sum_entries<DIM>(vals, s, e, gs, acc);
+    finish_row<DIM>(__ldg(keys + s), acc, weights, state, opt, d0, d1);
+  }
+}
+
+// piece_off[i] = exclusive prefix of pieces over the long list.
+__global__ void __launch_bounds__(1024)
+long_prefix_kernel(const uint32_t* __restrict__ long_list, const uint32_t* __restrict__ long_count,
+                   const uint32_t* __restrict__ starts, uint32_t* __restrict__ piece_off) {
+  __shared__ uint32_t s_warp[1024 / 32 + 1];
+  const uint32_t n = *long_count;
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < n; base += 1024) {
+    const uint32_t i = base + threadIdx.x;
+    uint32_t pieces = 0;
+    if (i < n) {
+      const uint32_t j = long_list[i];
+      pieces = (starts[j + 1] - starts[j] + kPiece - 1) / kPiece;
+    }
+    uint32_t total;
+    const uint32_t ex = block_exclusive_scan<1024>(pieces, s_warp, &total);
+    if (i < n) piece_off[i] = carry + ex;
+    carry += total;
+  }
+  if (threadIdx.x == 0) piece_off[n] = carry;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(kThreads)
+piece_kernel(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ starts,
+             const uint32_t* __restrict__ long_list, const uint32_t* __restrict__ long_count,
+             const uint32_t* __restrict__ piece_off, GradSource gs, float* __restrict__ partials) {
+  constexpr int VEC = DIM / 32;
+  const unsigned lane = threadIdx.x & 31u;
+  const uint32_t n = *long_count;
+  const uint32_t total = piece_off[n];
+  const uint32_t gwarp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
+  for (uint32_t p = gwarp; p < total; p += nwarps) {
+    uint32_t lo = 0, hi = n;  // last i with piece_off[i] <= p
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (piece_off[mid] <= p) lo = mid; else hi = mid;
+    }
+    const uint32_t j = long_list[lo];
+    const uint32_t seg_s = starts[j], seg_e = starts[j + 1];
+    const uint32_t s = seg_s + (p - piece_off[lo]) * kPiece;
+    const uint32_t e = min(s + kPiece, seg_e);
+    float acc[VEC];
+    sum_entries<DIM>(vals, s, e, gs, acc);
+    store_lane<VEC>(partials + static_cast<uint64_t>(p) * DIM + lane * VEC, acc);
+  }
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(kThreads)
+long_combine_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ starts,
+                    const uint32_t* __restrict__ long_list, const uint32_t* __restrict__ long_count,
+                    const uint32_t* __restrict__ piece_off, const float* __restrict__ partials,
+                    float* __restrict__ weights, float* __restrict__ state, OptParams opt,
+                    DenseRange d0, DenseRange d1) {
+  constexpr int VEC = DIM / 32;
+  constexpr int B = 8;
+  const unsigned lane = threadIdx.x & 31u;
+  const uint32_t n = *long_count;
+  const uint32_t gwarp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
+  for (uint32_t i = gwarp; i < n; i += nwarps) {
+    const uint32_t j = long_list[i];
+    const uint32_t p0 = piece_off[i], p1 = piece_off[i + 1];
+    float acc[VEC];
+    load_lane<VEC>(partials + static_cast<uint64_t>(p0) * DIM + lane * VEC, acc);
+    uint32_t p = p0 + 1;
+    for (; p + B <= p1; p += B) {
+      float r[B][VEC];
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        load_lane<VEC>(partials + static_cast<uint64_t>(p + b) * DIM + lane * VEC, r[b]);
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) acc[q] = __fadd_rn(acc[q], r[b][q]);
+      }
+    }
+    for (; p < p1; ++p) {
+      float r[VEC];
+      load_lane<VEC>(partials + static_cast<uint64_t>(p) * DIM + lane * VEC, r);
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) acc[q] = __fadd_rn(acc[q], r[q]);
+    }
+    finish_row<DIM>(keys[starts[j]], acc, weights, state, opt, d0, d1);
+  }
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(kThreads)
+dense_update_kernel(const float* __restrict__ grad, uint32_t rows, uint32_t row_lo,
+                    float* __restrict__ weights, float* __restrict__ state, OptParams opt) {
+  constexpr int VEC = DIM / 32;
+  const unsigned lane = threadIdx.x & 31u;
+  const uint32_t gwarp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
+  const DenseRange none{};
+  for (uint32_t r = gwarp; r < rows; r += nwarps) {
+    float g[VEC];
+    load_lane<VEC>(grad + static_cast<uint64_t>(r) * DIM + lane * VEC, g);
+    finish_row<DIM>(row_lo + r, g, weights, state, opt, none, none);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+init_weights_kernel(float* __restrict__ weights, uint64_t local_rows, uint32_t dim, uint64_t seed,
+                    const uint32_t* __restrict__ l2c) {
+  const uint64_t total = local_rows * dim;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += stride) {
+    const uint64_t l = i / dim;
+    const uint32_t d = static_cast<uint32_t>(i - l * dim);
+    const uint64_t canon = l2c ? l2c[l] : l;
+    weights[i] = init_weight(seed, canon, d, dim);
+  }
+}
+
+template <typename F>
+void dispatch_dim(uint32_t dim, F&& f) {
+  switch (dim) {
+    case 32: f(std::integral_constant<int, 32>{}); break;
+    case 64: f(std::integral_constant<int, 64>{}); break;
+    case 128: f(std::integral_constant<int, 128>{}); break;
+    case 256: f(std::integral_constant<int, 256>{}); break;
+    case 512: f(std::integral_constant<int, 512>{}); break;
+    case 1024: f(std::integral_constant<int, 1024>{}); break;
+    default:
+      fail(TS_ERR_CONFIG, "embedding_dim " + std::to_string(dim) +
+                              " unsupported by the device path (32, 64, 128, 256, 512, 1024)");
+  }
+}
+
+unsigned persistent_grid(unsigned per_sm = 8) { return static_cast<unsigned>(sm_count()) * per_sm; }
+
+}  // namespace
+
+unsigned gather_grid(uint64_t occ) {
+  const uint64_t want = (occ + 63) / 64;
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, persistent_grid(8))));
+}
+
+void launch_gather_local(const uint32_t* rows, uint64_t occ, const float* weights, float* out,
+                         const RemapView& remap, uint32_t dim, double* loss_partials,
+                         unsigned grid, cudaStream_t stream) {
+  dispatch_dim(dim, [&](auto D) {
+    constexpr int DIM = decltype(D)::value;
+    constexpr int UNROLL = DIM <= 128 ? 8 : (DIM <= 256 ? 4 : 2);
+    gather_local_kernel<DIM, UNROLL><<<grid, kThreads, 0, stream>>>(rows, occ, weights, out, remap,
+                                                                     loss_partials);
+  });
+  TSD_LAUNCH_CHECK();
+}
+
+void launch_loss_finalize(const double* partials, unsigned count, double* loss, cudaStream_t stream) {
+  loss_finalize_kernel<<<1, 1, 0, stream>>>(partials, count, loss);
+  TSD_LAUNCH_CHECK();
+}
+
+void launch_segment_update(const uint32_t* keys, const uint32_t* vals, const uint32_t* starts,
+                           const uint32_t* d_nseg, uint64_t n_entries, uint32_t dim,
+                           const GradSource& grads, float* weights, float* state,
+                           const OptParams& opt, const DenseRange& dense0,
+                           const DenseRange& dense1, const SegmentScratch& sc,
+                           cudaStream_t stream) {
+  if (n_entries == 0) return;
+  TSD_CUDA(cudaMemsetAsync(sc.long_count, 0, sizeof(uint32_t), stream));
+  const unsigned grid = persistent_grid(8);
+  dispatch_dim(dim, [&](auto D) {
+    constexpr int DIM = decltype(D)::value;
+    seg_short_kernel<DIM><<<grid, kThreads, 0, stream>>>(keys, vals, starts, d_nseg, grads, weights,
+                                                         state, opt, dense0, dense1, sc.long_list,
+                                                         sc.long_count);
+    TSD_LAUNCH_CHECK();
+    long_prefix_kernel<<<1, 1024, 0, stream>>>(sc.long_list, sc.long_count, starts, sc.piece_off);
+    TSD_LAUNCH_CHECK();
+    piece_kernel<DIM><<<grid, kThreads, 0, stream>>>(vals, starts, sc.long_list, sc.long_count,
+                                                     sc.piece_off, grads, sc.partials);
+    TSD_LAUNCH_CHECK();
+    long_combine_kernel<DIM><<<grid, kThreads, 0, stream>>>(keys, starts, sc.long_list,
+                                                            sc.long_count, sc.piece_off,
+                                                            sc.partials, weights, state, opt,
+                                                            dense0, dense1);
+    TSD_LAUNCH_CHECK();
+  });
+}
+
+void launch_dense_update(const float* grad, uint32_t rows, uint32_t row_lo, uint32_t dim,
+                         float* weights, float* state, const OptParams& opt, cudaStream_t stream) {
+  if (rows == 0) return;
+  const unsigned grid = std::min<unsigned>(persistent_grid(8), ceil_div(rows, kThreads / 32));
+  dispatch_dim(dim, [&](auto D) {
+    constexpr int DIM = decltype(D)::value;
+    dense_update_kernel<DIM><<<grid, kThreads, 0, stream>>>(grad, rows, row_lo, weights, state, opt);
+  });
+  TSD_LAUNCH_CHECK();
+}
+
+void launch_init_weights(float* weights, uint64_t local_rows, uint32_t dim, uint64_t seed,
+                         const uint32_t* l2c, cudaStream_t stream) {
+  if (local_rows == 0) return;
+  init_weights_kernel<<<persistent_grid(8), kThreads, 0, stream>>>(weights, local_rows, dim, seed, l2c);
+  TSD_LAUNCH_CHECK();
+}
+
+}  // namespace tsd

@@ -1,0 +1,88 @@
+// Value-path kernels of the tiered sequence embedding: unpooled gather,
+// deterministic segment reduction of gradients and the fused row-wise
+// optimizer.  Contract (bit-for-bit on one GPU): oracle/restate.h.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tsd {
+
+// Pieces of a long segment: ORC_PIECE in the oracle.
+constexpr uint32_t kPiece = 256;
+
+// How a requester finds the local shard row of a canonical row (or learns it
+// is served remotely).  identity: U == 1, local id == canonical index.
+struct RemapView {
+  const uint8_t* dest = nullptr;    // [n] RW owner / Flex slot
+  const uint32_t* local = nullptr;  // [n] local id at the serving rank
+  uint64_t dp_cut = 0, flex_cut = 0;
+  uint32_t rank = 0;   // g
+  uint32_t slot = 0;   // g % W
+  bool identity = true;
+};
+
+struct OptParams {
+  int optimizer = 0;  // TS_OPT_*
+  float lr = 0.01f;
+  float eps = 1e-8f;
+};
+
+// Rows in [dense_lo, dense_hi) are not updated in place: their reduced
+// gradient is written to dense_grad[row - dense_lo] (all-reduced later).
+struct DenseRange {
+  uint32_t lo = 0, hi = 0;
+  float* grad = nullptr;
+};
+
+// Gradient source of sorted entry value v: v < n_local -> local grads
+// [n_local x dim], else remote grads [(v - n_local) x dim].
+struct GradSource {
+  const float* local = nullptr;
+  const float* remote = nullptr;
+  uint32_t n_local = 0;
+};
+
+// out[i] = W[local(rows[i])] for every occurrence served locally; remote
+// occurrences are skipped (filled by the exchange).  Writes per-block
+// partial sums of out^2 (double) into loss_partials[gridDim.x].
+void launch_gather_local(const uint32_t* rows, uint64_t occ, const float* weights, float* out,
+                         const RemapView& remap, uint32_t dim, double* loss_partials,
+                         unsigned grid, cudaStream_t stream);
+unsigned gather_grid(uint64_t occ);
+
+// Final fixed-order reduction of the loss partials: *loss = 0.5 * sum.
+void launch_loss_finalize(const double* partials, unsigned count, double* loss,
+                          cudaStream_t stream);
+
+// Segment reduction + optimizer over sorted (keys, vals) with segment starts.
+// Short segments (<= kPiece entries) are reduced and applied by one warp;
+// longer ones are split into kPiece pieces reduced in parallel and combined
+// in piece order.  long_list / piece_off / partials are scratch sized by
+// max_long (segments) and max_pieces (pieces) — see DESIGN.md.
+struct SegmentScratch {
+  uint32_t* long_list = nullptr;   // max_long
+  uint32_t* long_count = nullptr;  // 1 (+ pad)
+  uint32_t* piece_off = nullptr;   // max_long + 1
+  float* partials = nullptr;       // max_pieces * dim
+  uint32_t max_long = 0;
+  uint32_t max_pieces = 0;
+};
+
+void launch_segment_update(const uint32_t* keys, const uint32_t* vals, const uint32_t* starts,
+                           const uint32_t* d_nseg, uint64_t n_entries, uint32_t dim,
+                           const GradSource& grads, float* weights, float* state,
+                           const OptParams& opt, const DenseRange& dense0,
+                           const DenseRange& dense1, const SegmentScratch& scratch,
+                           cudaStream_t stream);
+
+// Dense optimizer over rows [row_lo, row_lo + rows) with gradients g[rows x dim].
+void launch_dense_update(const float* grad, uint32_t rows, uint32_t row_lo, uint32_t dim,
+                         float* weights, float* state, const OptParams& opt, cudaStream_t stream);
+
+// weights[l, d] = init_weight(seed, canon(l), d); canon = l when l2c == nullptr.
+void launch_init_weights(float* weights, uint64_t local_rows, uint32_t dim, uint64_t seed,
+                         const uint32_t* l2c, cudaStream_t stream);
+
+}  // namespace tsd

@@ -1,0 +1,842 @@
+// ts_table_*: one rank's shard of the per-row tiered sequence-embedding table
+// and its lookup (forward) / update (backward) entry points.
+//
+// HBM layout of rank g:
+//   weights [local_rows x dim] fp32 = [DP rows 0..dp_cut) | Flex rows of slot
+//   g%W | RW rows owned by g], each group in canonical order; Adagrad state
+//   [local_rows] fp32; remap u32[n] + placement byte u8[n] (U > 1 only — with
+//   U == 1 the local id IS the canonical index and no remap is stored).
+//
+// Forward (U == 1): one fused gather over all occurrences.
+// Forward (U > 1): bucket (DP/own -> local, RW -> owner, Flex -> node slot),
+//   stable counting pass to compact remote occurrences per destination, count
+//   all-gather + one D2H sync, NCCL all-to-allv of ids (world comm for RW,
+//   intra comm g/W for Flex), server-side gather, all-to-allv of rows back,
+//   scatter into the unpooled output.  Local occurrences are gathered
+//   directly while the exchange is in flight on the same stream order.
+// Backward: grads of remote occurrences go back to their servers (reverse
+//   all-to-allv); each server sorts (local row, source) pairs in ascending
+//   source-rank / occurrence order, segment-reduces, and applies the fused
+//   optimizer; DP rows (world) and, with N > 1, Flex rows (cross comm g%W)
+//   are reduced into dense buffers, all-reduced, then updated identically on
+//   every replica.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <array>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "embedding.cuh"
+#include "primitives.cuh"
+#include "route.cuh"
+
+namespace tsd {
+namespace {
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) {
+    fail(TS_ERR_NCCL, std::string("NCCL error in ") + what + ": " + ncclGetErrorString(r));
+  }
+}
+#define TSD_NCCL(call) ::tsd::nccl_check((call), #call)
+
+template <typename T>
+struct DevBuf {
+  T* ptr = nullptr;
+  uint64_t cap = 0;
+  void ensure(uint64_t n) {
+    if (n <= cap && ptr) return;
+    if (ptr) TSD_CUDA(cudaFree(ptr));
+    ptr = nullptr;
+    cap = std::max<uint64_t>(n, 1);
+    TSD_CUDA(cudaMalloc(&ptr, sizeof(T) * cap));
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+};
+
+int bits_for(uint64_t max_value) {
+  int b = 1;
+  while (b < 32 && (uint64_t{1} << b) <= max_value) ++b;
+  return b;
+}
+
+enum Phase : int {
+  kPhaseRoute = 0,
+  kPhaseGather,
+  kPhaseExchangeFwd,
+  kPhaseScatter,
+  kPhaseExchangeBwd,
+  kPhaseSort,
+  kPhaseSegments,
+  kPhaseSegmentUpdate,
+  kPhaseAllReduce,
+  kPhaseDenseUpdate,
+  kNumPhases
+};
+
+const char* const kPhaseNames[kNumPhases] = {
+    "route",         "gather",         "exchange_fwd", "scatter",  "exchange_bwd",
+    "dedup_sort",    "segment_starts", "segment_update", "allreduce", "dense_update"};
+
+}  // namespace
+}  // namespace tsd
+
+struct ts_table {
+  ts_table_config cfg{};
+  uint32_t U = 1, W = 1, N = 1, g = 0, slot = 0, node = 0;
+  cudaStream_t stream = nullptr;
+  ncclComm_t world = nullptr, intra = nullptr, cross = nullptr;
+
+  // shard
+  uint64_t local_rows = 0, dp_rows = 0, flex_rows = 0, rw_rows = 0;
+  float* d_w = nullptr;
+  float* d_state = nullptr;
+  uint8_t* d_dest = nullptr;
+  uint32_t* d_local = nullptr;
+  std::vector<uint32_t> h_local;  // canonical -> local id (U > 1)
+  std::vector<uint8_t> h_dest;
+
+  // step state
+  const uint32_t* last_rows = nullptr;
+  uint64_t last_occ = 0;
+  float* last_out = nullptr;
+  unsigned gather_grid = 0;
+
+  tsd::DevBuf<double> loss_partials, d_loss;
+  tsd::DevBuf<unsigned long long> tier_counts;  // RW, Flex, DP of this requester
+  tsd::DevBuf<uint32_t> rows_dev;                // host-step staging
+  // dedup / sort
+  tsd::DevBuf<uint32_t> keys_a, vals_a, keys_b, vals_b, hist, hist_scan, scan_scratch;
+  tsd::DevBuf<uint32_t> starts, seg_scratch, nseg;
+  tsd::DevBuf<uint32_t> long_list, long_count, piece_off, entry_keys, entry_vals;
+  tsd::DevBuf<float> partials;
+  // U > 1 routing / exchange
+  tsd::DevBuf<uint32_t> bucket, order, send_ids, recv_ids, bucket_start, all_counts;
+  tsd::DevBuf<float> send_rows, recv_rows, dense_dp, dense_flex;
+  std::vector<uint32_t> h_counts;     // [U][NB] send counts of every rank
+  std::vector<uint64_t> send_off, send_cnt, recv_off, recv_cnt;  // per peer (entries)
+  uint64_t n_remote = 0, n_local_occ = 0, recv_total = 0, recv_before = 0;
+  uint64_t last_entries = 0;
+  std::array<uint64_t, 3> last_tiers{};  // RW, Flex, DP (host, after sync)
+
+  // timing
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+  std::vector<std::pair<int, int>> ev_used;  // (phase, pool index)
+  double phase_ms[tsd::kNumPhases] = {};
+  uint64_t phase_launches[tsd::kNumPhases] = {};
+
+  uint32_t nb() const { return U + W + 1; }  // buckets incl. the local one
+
+  // --- timing helpers --------------------------------------------------------
+  int phase_begin(int phase) {
+    if (!timing) return -1;
+    const size_t idx = ev_used.size();
+    if (idx >= ev_pool.size()) {
+      cudaEvent_t a, b;
+      TSD_CUDA(cudaEventCreate(&a));
+      TSD_CUDA(cudaEventCreate(&b));
+      ev_pool.emplace_back(a, b);
+    }
+    TSD_CUDA(cudaEventRecord(ev_pool[idx].first, stream));
+    ev_used.emplace_back(phase, static_cast<int>(idx));
+    return static_cast<int>(idx);
+  }
+  void phase_end(int token) {
+    if (token < 0) return;
+    TSD_CUDA(cudaEventRecord(ev_pool[token].second, stream));
+  }
+  void collect_timing() {
+    if (ev_used.empty()) return;
+    TSD_CUDA(cudaStreamSynchronize(stream));
+    for (const auto& [phase, idx] : ev_used) {
+      float ms = 0.f;
+      TSD_CUDA(cudaEventElapsedTime(&ms, ev_pool[idx].first, ev_pool[idx].second));
+      phase_ms[phase] += ms;
+      phase_launches[phase] += 1;
+    }
+    ev_used.clear();
+  }
+
+  tsd::RemapView remap_view() const {
+    tsd::RemapView rv;
+    rv.identity = U == 1;
+    rv.dest = d_dest;
+    rv.local = d_local;
+    rv.dp_cut = cfg.dp_cut;
+    rv.flex_cut = cfg.flex_cut;
+    rv.rank = g;
+    rv.slot = slot;
+    return rv;
+  }
+
+  void ensure_sort_capacity(uint64_t m) {
+    keys_a.ensure(m);
+    vals_a.ensure(m);
+    keys_b.ensure(m);
+    vals_b.ensure(m);
+    const uint64_t tiles = tsd::radix_tiles(m);
+    hist.ensure(tiles * tsd::kRadixBins);
+    hist_scan.ensure(tiles * tsd::kRadixBins);
+    scan_scratch.ensure(tsd::scan_scratch_elems(tiles * tsd::kRadixBins) + 1);
+    starts.ensure(m + 1);
+    seg_scratch.ensure(tsd::segment_scratch_elems(m) + 8);
+    const uint64_t max_long = m / (tsd::kPiece + 1) + 1;
+    long_list.ensure(max_long);
+    piece_off.ensure(max_long + 1);
+    partials.ensure((m / tsd::kPiece + max_long + 1) * cfg.dim);
+  }
+
+  // ------------------------------------------------------------------------
+  void create(const ts_table_config& c, const uint8_t* tier_dest);
+  void forward(const uint32_t* d_rows, uint64_t occ, float* d_out);
+  void backward(const float* d_grad);
+  void exchange(const void* send, const std::vector<uint64_t>& s_off,
+                const std::vector<uint64_t>& s_cnt, void* recv,
+                const std::vector<uint64_t>& r_off, const std::vector<uint64_t>& r_cnt,
+                size_t elem_bytes, bool flex_part_only_intra);
+  void destroy();
+};
+
+// ---------------------------------------------------------------------------
+// create
+// ---------------------------------------------------------------------------
+
+void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
+  using namespace tsd;
+  cfg = c;
+  N = c.num_nodes;
+  W = c.gpus_per_node;
+  U = N * W;
+  g = c.rank;
+  slot = g % W;
+  node = g / W;
+  if (N == 0 || W == 0 || U > 256) fail(TS_ERR_CONFIG, "table: need 1 <= N*W <= 256 GPUs");
+  if (g >= U) fail(TS_ERR_CONFIG, "table: rank out of range");
+  if (c.dim == 0 || c.dim % 32 != 0 || c.dim > 1024 || (c.dim & (c.dim - 1)) != 0) {
+    fail(TS_ERR_CONFIG, "embedding_dim " + std::to_string(c.dim) +
+                            " unsupported by the device path (32, 64, 128, 256, 512, 1024)");
+  }
+  if (c.n_rows == 0 || c.n_rows > 0xFFFFFFFFull) fail(TS_ERR_VALIDATION, "table: need 1 <= rows < 2^32");
+  if (c.dp_cut > c.flex_cut || c.flex_cut > c.n_rows) {
+    fail(TS_ERR_VALIDATION, "assign_rows: plan does not cover the distribution");
+  }
+  if (c.optimizer != TS_OPT_SGD && c.optimizer != TS_OPT_ROWWISE_ADAGRAD) {
+    fail(TS_ERR_CONFIG, "table: unknown optimizer");
+  }
+  if (c.max_occurrences == 0 || c.max_occurrences >= 0x7FFFFFFFull) {
+    fail(TS_ERR_CONFIG, "table: max_occurrences must be in [1, 2^31)");
+  }
+  if (U > 1 && !c.nccl_unique_id) fail(TS_ERR_CONFIG, "table: U > 1 needs an NCCL unique id");
+  if (U > 1 && !tier_dest) fail(TS_ERR_CONFIG, "table: U > 1 needs the placement table");
+  use_device(c.device);
+  TSD_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+
+  // ---- local layout --------------------------------------------------------
+  std::vector<uint32_t> l2c;
+  if (U == 1) {
+    dp_rows = c.dp_cut;
+    flex_rows = c.flex_cut - c.dp_cut;
+    rw_rows = c.n_rows - c.flex_cut;
+    local_rows = c.n_rows;
+  } else {
+    const uint64_t n = c.n_rows;
+    h_dest.assign(tier_dest, tier_dest + n);
+    std::vector<uint64_t> flex_total(W, 0), rw_total(U, 0);
+    for (uint64_t i = c.dp_cut; i < c.flex_cut; ++i) {
+      if (tier_dest[i] >= W) fail(TS_ERR_VALIDATION, "table: Flex slot byte out of range");
+      ++flex_total[tier_dest[i]];
+    }
+    for (uint64_t i = c.flex_cut; i < n; ++i) {
+      if (tier_dest[i] >= U) fail(TS_ERR_VALIDATION, "table: RW owner byte out of range");
+      ++rw_total[tier_dest[i]];
+    }
+    h_local.assign(n, 0);
+    std::vector<uint64_t> flex_next(W, 0), rw_next(U, 0);
+    for (uint64_t i = 0; i < c.dp_cut; ++i) h_local[i] = static_cast<uint32_t>(i);
+    for (uint64_t i = c.dp_cut; i < c.flex_cut; ++i) {
+      h_local[i] = static_cast<uint32_t>(c.dp_cut + flex_next[tier_dest[i]]++);
+    }
+    for (uint64_t i = c.flex_cut; i < n; ++i) {
+      const uint8_t o = tier_dest[i];
+      h_local[i] = static_cast<uint32_t>(c.dp_cut + flex_total[o % W] + rw_next[o]++);
+    }
+    dp_rows = c.dp_cut;
+    flex_rows = flex_total[slot];
+    rw_rows = rw_total[g];
+    local_rows = dp_rows + flex_rows + rw_rows;
+    l2c.resize(local_rows);
+    for (uint64_t i = 0; i < c.dp_cut; ++i) l2c[i] = static_cast<uint32_t>(i);
+    for (uint64_t i = c.dp_cut; i < c.flex_cut; ++i) {
+      if (tier_dest[i] == slot) l2c[h_local[i]] = static_cast<uint32_t>(i);
+    }
+    for (uint64_t i = c.flex_cut; i < n; ++i) {
+      if (tier_dest[i] == g) l2c[h_local[i]] = static_cast<uint32_t>(i);
+    }
+    TSD_CUDA(cudaMalloc(&d_dest, n));
+    TSD_CUDA(cudaMalloc(&d_local, sizeof(uint32_t) * n));
+    TSD_CUDA(cudaMemcpyAsync(d_dest, tier_dest, n, cudaMemcpyHostToDevice, stream));
+    TSD_CUDA(cudaMemcpyAsync(d_local, h_local.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice,
+                             stream));
+  }
+
+  TSD_CUDA(cudaMalloc(&d_w, sizeof(float) * std::max<uint64_t>(local_rows, 1) * c.dim));
+  if (c.optimizer == TS_OPT_ROWWISE_ADAGRAD) {
+    TSD_CUDA(cudaMalloc(&d_state, sizeof(float) * std::max<uint64_t>(local_rows, 1)));
+    TSD_CUDA(cudaMemsetAsync(d_state, 0, sizeof(float) * std::max<uint64_t>(local_rows, 1), stream));
+  }
+  {
+    DevBuf<uint32_t> d_l2c;
+    if (!l2c.empty()) {
+      d_l2c.ensure(l2c.size());
+      TSD_CUDA(cudaMemcpyAsync(d_l2c.ptr, l2c.data(), sizeof(uint32_t) * l2c.size(),
+                               cudaMemcpyHostToDevice, stream));
+    }
+    launch_init_weights(d_w, local_rows, c.dim, c.weight_seed, l2c.empty() ? nullptr : d_l2c.ptr,
+                        stream);
+    TSD_CUDA(cudaStreamSynchronize(stream));
+    d_l2c.release();
+  }
+
+  // ---- step buffers ----------------------------------------------------------
+  gather_grid = tsd::gather_grid(c.max_occurrences);
+  loss_partials.ensure(2 * gather_grid);
+  d_loss.ensure(1);
+  tier_counts.ensure(4);
+  nseg.ensure(4);
+  long_count.ensure(4);
+  ensure_sort_capacity(c.max_occurrences);
+  if (U > 1) {
+    bucket.ensure(c.max_occurrences);
+    order.ensure(c.max_occurrences);
+    send_ids.ensure(c.max_occurrences);
+    send_rows.ensure(c.max_occurrences * c.dim);
+    bucket_start.ensure(nb() + 2);
+    all_counts.ensure(static_cast<uint64_t>(U) * (nb() + 1));
+    dense_dp.ensure(std::max<uint64_t>(dp_rows, 1) * c.dim);
+    if (N > 1) dense_flex.ensure(std::max<uint64_t>(flex_rows, 1) * c.dim);
+    // communicators: world, intra (color = node), cross (color = slot)
+    ncclUniqueId id;
+    std::memcpy(&id, c.nccl_unique_id, sizeof(id));
+    TSD_NCCL(ncclCommInitRank(&world, static_cast<int>(U), id, static_cast<int>(g)));
+    TSD_NCCL(ncclCommSplit(world, static_cast<int>(node), static_cast<int>(g), &intra, nullptr));
+    TSD_NCCL(ncclCommSplit(world, static_cast<int>(slot), static_cast<int>(g), &cross, nullptr));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// NCCL all-to-allv: per-peer offsets/counts in elements of elem_bytes.
+// RW traffic rides `world`; Flex traffic rides `intra` (peer = node slot).
+// The per-peer buffers are laid out [peer p: RW part | Flex part].
+// ---------------------------------------------------------------------------
+
+void ts_table::exchange(const void* send, const std::vector<uint64_t>& s_off,
+                        const std::vector<uint64_t>& s_cnt, void* recv,
+                        const std::vector<uint64_t>& r_off, const std::vector<uint64_t>& r_cnt,
+                        size_t elem_bytes, bool /*unused*/) {
+  // s_off/s_cnt/r_off/r_cnt have 2*U entries: [p*2 + 0] RW, [p*2 + 1] Flex.
+  auto* sb = static_cast<const char*>(send);
+  auto* rb = static_cast<char*>(recv);
+  TSD_NCCL(ncclGroupStart());
+  for (uint32_t p = 0; p < U; ++p) {
+    if (p == g) continue;
+    const size_t s0 = s_cnt[2 * p] * elem_bytes, r0 = r_cnt[2 * p] * elem_bytes;
+    if (s0) TSD_NCCL(ncclSend(sb + s_off[2 * p] * elem_bytes, s0, ncclChar, static_cast<int>(p), world, stream));
+    if (r0) TSD_NCCL(ncclRecv(rb + r_off[2 * p] * elem_bytes, r0, ncclChar, static_cast<int>(p), world, stream));
+  }
+  for (uint32_t p = node * W; p < (node + 1) * W; ++p) {
+    if (p == g) continue;
+    const int peer = static_cast<int>(p % W);  // rank inside the intra comm
+    const size_t s1 = s_cnt[2 * p + 1] * elem_bytes, r1 = r_cnt[2 * p + 1] * elem_bytes;
+    if (s1) TSD_NCCL(ncclSend(sb + s_off[2 * p + 1] * elem_bytes, s1, ncclChar, peer, intra, stream));
+    if (r1) TSD_NCCL(ncclRecv(rb + r_off[2 * p + 1] * elem_bytes, r1, ncclChar, peer, intra, stream));
+  }
+  TSD_NCCL(ncclGroupEnd());
+}
+
+// ---------------------------------------------------------------------------
+// forward
+// ---------------------------------------------------------------------------
+
+void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
+  using namespace tsd;
+  if (occ > cfg.max_occurrences) fail(TS_ERR_VALIDATION, "table: batch exceeds max_occurrences");
+  last_rows = d_rows;
+  last_occ = occ;
+  last_out = d_out;
+  const RemapView rv = remap_view();
+  TSD_CUDA(cudaMemsetAsync(tier_counts.ptr, 0, sizeof(unsigned long long) * 4, stream));
+
+  if (U == 1) {
+    int t = phase_begin(kPhaseGather);
+    launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, gather_grid, stream);
+    phase_end(t);
+    launch_loss_finalize(loss_partials.ptr, gather_grid, d_loss.ptr, stream);
+    n_local_occ = occ;
+    n_remote = 0;
+    return;
+  }
+
+  // ---- route: bucket + stable compaction of remote occurrences -------------
+  int t = phase_begin(kPhaseRoute);
+  BucketView bv;
+  bv.dest = d_dest;
+  bv.dp_cut = cfg.dp_cut;
+  bv.flex_cut = cfg.flex_cut;
+  bv.u = U;
+  bv.w = W;
+  bv.rank = g;
+  bv.slot = slot;
+  launch_bucket_keys(d_rows, occ, bv, bucket.ptr, tier_counts.ptr, stream);
+  RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, hist.ptr, hist_scan.ptr,
+                  scan_scratch.ptr};
+  uint32_t* sorted_b = nullptr;
+  uint32_t* sorted_i = nullptr;
+  radix_sort_pairs(bucket.ptr, nullptr, occ, bits_for(nb() - 1), rb, &sorted_b, &sorted_i, stream);
+  // keep the occurrence order for backward (sort buffers are reused)
+  TSD_CUDA(cudaMemcpyAsync(order.ptr, sorted_i, sizeof(uint32_t) * occ, cudaMemcpyDeviceToDevice, stream));
+  phase_end(t);
+
+  // ---- counts: every rank's bucket starts, all-gathered, one D2H sync -----
+  {
+    const int passes = (bits_for(nb() - 1) + 7) / 8;
+    if (passes != 1) fail(TS_ERR_CONFIG, "table: U + W + 1 must be <= 256 buckets");
+    launch_bucket_starts(hist_scan.ptr, radix_tiles(occ), nb(), static_cast<uint32_t>(occ),
+                         bucket_start.ptr, stream);
+    TSD_NCCL(ncclAllGather(bucket_start.ptr, all_counts.ptr, nb() + 1, ncclUint32, world, stream));
+    h_counts.resize(static_cast<size_t>(U) * (nb() + 1));
+    TSD_CUDA(cudaMemcpyAsync(h_counts.data(), all_counts.ptr, sizeof(uint32_t) * U * (nb() + 1),
+                             cudaMemcpyDeviceToHost, stream));
+    TSD_CUDA(cudaStreamSynchronize(stream));
+  }
+  // h_counts holds every rank's bucket starts ([rank][nb + 1]); bucket b of
+  // rank p spans [start(p,b), start(p,b+1)), start(p, nb) == that rank's occ.
+  auto start_of = [&](uint32_t p, uint32_t b) -> uint64_t {
+    return h_counts[size_t{p} * (nb() + 1) + b];
+  };
+  auto count_of = [&](uint32_t p, uint32_t b) -> uint64_t { return start_of(p, b + 1) - start_of(p, b); };
+  const uint32_t local_b = U + W;
+  n_remote = start_of(g, local_b);
+  n_local_occ = occ - n_remote;
+
+  // send layout: per peer [RW part | Flex part] taken from my buckets; my
+  // remote buckets are contiguous in bucket order, which is exactly
+  // RW-by-server then Flex-by-slot.  NCCL gets per-peer offsets directly.
+  send_off.assign(2 * U, 0);
+  send_cnt.assign(2 * U, 0);
+  recv_off.assign(2 * U, 0);
+  recv_cnt.assign(2 * U, 0);
+  for (uint32_t p = 0; p < U; ++p) {
+    send_off[2 * p] = start_of(g, p);
+    send_cnt[2 * p] = p == g ? 0 : count_of(g, p);
+    if (p / W == node && p != g) {
+      send_off[2 * p + 1] = start_of(g, U + p % W);
+      send_cnt[2 * p + 1] = count_of(g, U + p % W);
+    }
+  }
+  // receive layout ordered by source rank: [p: RW from p | Flex from p]
+  uint64_t acc = 0;
+  recv_before = 0;
+  for (uint32_t p = 0; p < U; ++p) {
+    if (p == g) {
+      recv_before = acc;
+      continue;
+    }
+    recv_off[2 * p] = acc;
+    recv_cnt[2 * p] = count_of(p, g);
+    acc += recv_cnt[2 * p];
+    if (p / W == node) {
+      recv_off[2 * p + 1] = acc;
+      recv_cnt[2 * p + 1] = count_of(p, U + slot);
+      acc += recv_cnt[2 * p + 1];
+    }
+  }
+  recv_total = acc;
+  recv_ids.ensure(recv_total);
+  recv_rows.ensure(recv_total * cfg.dim);
+
+  // ---- ids of remote occurrences, exchange ---------------------------------
+  launch_remote_ids(d_rows, order.ptr, n_remote, d_local, send_ids.ptr, stream);
+  t = phase_begin(kPhaseExchangeFwd);
+  exchange(send_ids.ptr, send_off, send_cnt, recv_ids.ptr, recv_off, recv_cnt, sizeof(uint32_t), false);
+  phase_end(t);
+
+  // ---- local gather (DP + own shard) ---------------------------------------
+  t = phase_begin(kPhaseGather);
+  launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, gather_grid, stream);
+  // server side: rows requested by peers, in received order
+  launch_copy_rows(d_w, recv_ids.ptr, recv_rows.ptr, nullptr, recv_total, cfg.dim, stream);
+  phase_end(t);
+
+  // ---- rows back to requesters ---------------------------------------------
+  t = phase_begin(kPhaseExchangeFwd);
+  exchange(recv_rows.ptr, recv_off, recv_cnt, send_rows.ptr, send_off, send_cnt,
+           sizeof(float) * cfg.dim, false);
+  phase_end(t);
+  t = phase_begin(kPhaseScatter);
+  launch_scatter_rows_loss(send_rows.ptr, d_out, order.ptr, n_remote, cfg.dim,
+                           loss_partials.ptr + gather_grid, gather_grid, stream);
+  phase_end(t);
+  // loss = local-gather partials + scatter partials, fixed order
+  launch_loss_finalize(loss_partials.ptr, 2 * gather_grid, d_loss.ptr, stream);
+}
+
+// ---------------------------------------------------------------------------
+// backward
+// ---------------------------------------------------------------------------
+
+void ts_table::backward(const float* d_grad) {
+  using namespace tsd;
+  if (!last_rows && last_occ) fail(TS_ERR_VALIDATION, "table: backward without forward");
+  const uint64_t occ = last_occ;
+  const RemapView rv = remap_view();
+  OptParams opt;
+  opt.optimizer = cfg.optimizer;
+  opt.lr = cfg.lr;
+  opt.eps = cfg.eps;
+  DenseRange d0, d1;
+  GradSource gs;
+  gs.local = d_grad;
+  gs.n_local = static_cast<uint32_t>(occ);
+
+  const uint32_t* keys_in = nullptr;
+  const uint32_t* vals_in = nullptr;
+  uint64_t m = occ;
+  if (U == 1) {
+    keys_in = last_rows;  // local id == canonical index; vals = iota
+  } else {
+    // grads of remote occurrences -> servers (reverse of the row exchange)
+    int t = phase_begin(kPhaseExchangeBwd);
+    launch_copy_rows(d_grad, order.ptr, send_rows.ptr, nullptr, n_remote, cfg.dim, stream);
+    exchange(send_rows.ptr, send_off, send_cnt, recv_rows.ptr, recv_off, recv_cnt,
+             sizeof(float) * cfg.dim, false);
+    phase_end(t);
+    gs.remote = recv_rows.ptr;
+    m = n_local_occ + recv_total;
+    entry_keys.ensure(m);
+    entry_vals.ensure(m);
+    ensure_sort_capacity(m);
+    launch_build_entries(last_rows, order.ptr + n_remote, n_local_occ, rv, recv_ids.ptr, recv_before,
+                         recv_total, static_cast<uint32_t>(occ), entry_keys.ptr, entry_vals.ptr,
+                         stream);
+    keys_in = entry_keys.ptr;
+    vals_in = entry_vals.ptr;
+    if (dp_rows) {
+      d0.lo = 0;
+      d0.hi = static_cast<uint32_t>(dp_rows);
+      d0.grad = dense_dp.ptr;
+      TSD_CUDA(cudaMemsetAsync(dense_dp.ptr, 0, sizeof(float) * dp_rows * cfg.dim, stream));
+    }
+    if (N > 1 && flex_rows) {
+      d1.lo = static_cast<uint32_t>(dp_rows);
+      d1.hi = static_cast<uint32_t>(dp_rows + flex_rows);
+      d1.grad = dense_flex.ptr;
+      TSD_CUDA(cudaMemsetAsync(dense_flex.ptr, 0, sizeof(float) * flex_rows * cfg.dim, stream));
+    }
+  }
+  last_entries = m;
+
+  int t = phase_begin(kPhaseSort);
+  RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, hist.ptr, hist_scan.ptr,
+                  scan_scratch.ptr};
+  uint32_t* sk = nullptr;
+  uint32_t* sv = nullptr;
+  radix_sort_pairs(keys_in, vals_in, m, bits_for(local_rows ? local_rows - 1 : 0), rb, &sk, &sv, stream);
+  phase_end(t);
+  t = phase_begin(kPhaseSegments);
+  segment_starts(sk, m, starts.ptr, nseg.ptr, seg_scratch.ptr, stream);
+  phase_end(t);
+  t = phase_begin(kPhaseSegmentUpdate);
+  SegmentScratch sc;
+  sc.long_list = long_list.ptr;
+  sc.long_count = long_count.ptr;
+  sc.piece_off = piece_off.ptr;
+  sc.partials = partials.ptr;
+  launch_segment_update(sk, sv, starts.ptr, nseg.ptr, m, cfg.dim, gs, d_w, d_state, opt, d0, d1, sc,
+                        stream);
+  phase_end(t);
+
+  if (U > 1) {
+    t = phase_begin(kPhaseAllReduce);
+    TSD_NCCL(ncclGroupStart());
+    if (dp_rows) {
+      TSD_NCCL(ncclAllReduce(dense_dp.ptr, dense_dp.ptr, dp_rows * cfg.dim, ncclFloat32, ncclSum, world,
+                             stream));
+    }
+    if (N > 1 && flex_rows) {
+      TSD_NCCL(ncclAllReduce(dense_flex.ptr, dense_flex.ptr, flex_rows * cfg.dim, ncclFloat32, ncclSum,
+                             cross, stream));
+    }
+    TSD_NCCL(ncclGroupEnd());
+    phase_end(t);
+    t = phase_begin(kPhaseDenseUpdate);
+    if (dp_rows) {
+      launch_dense_update(dense_dp.ptr, static_cast<uint32_t>(dp_rows), 0, cfg.dim, d_w, d_state, opt,
+                          stream);
+    }
+    if (N > 1 && flex_rows) {
+      launch_dense_update(dense_flex.ptr, static_cast<uint32_t>(flex_rows),
+                          static_cast<uint32_t>(dp_rows), cfg.dim, d_w, d_state, opt, stream);
+    }
+    phase_end(t);
+  }
+}
+
+void ts_table::destroy() {
+  cudaSetDevice(cfg.device);
+  if (stream) cudaStreamSynchronize(stream);
+  if (world) ncclCommDestroy(world);
+  if (intra) ncclCommDestroy(intra);
+  if (cross) ncclCommDestroy(cross);
+  cudaFree(d_w);
+  cudaFree(d_state);
+  cudaFree(d_dest);
+  cudaFree(d_local);
+  for (auto* b : {&loss_partials}) b->release();
+  d_loss.release();
+  tier_counts.release();
+  rows_dev.release();
+  for (auto* b : {&keys_a, &vals_a, &keys_b, &vals_b, &hist, &hist_scan, &scan_scratch, &starts,
+                  &seg_scratch, &nseg, &long_list, &long_count, &piece_off, &entry_keys,
+                  &entry_vals, &bucket, &order, &send_ids, &recv_ids, &bucket_start, &all_counts}) {
+    b->release();
+  }
+  for (auto* b : {&partials, &send_rows, &recv_rows, &dense_dp, &dense_flex}) b->release();
+  for (auto& [a, b] : ev_pool) {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  if (stream) cudaStreamDestroy(stream);
+}
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+ts_status ts_table_create(ts_table** out, const ts_table_config* cfg, const uint8_t* tier_dest) {
+  return tsd::guarded([&] {
+    if (!out || !cfg) tsd::fail(TS_ERR_CONFIG, "ts_table_create: null argument");
+    *out = nullptr;
+    auto t = std::make_unique<ts_table>();
+    try {
+      t->create(*cfg, tier_dest);
+    } catch (...) {
+      t->destroy();
+      throw;
+    }
+    *out = t.release();
+  });
+}
+
+ts_status ts_table_destroy(ts_table* t) {
+  return tsd::guarded([&] {
+    if (!t) return;
+    t->destroy();
+    delete t;
+  });
+}
+
+ts_status ts_table_shard_rows(ts_table* t, uint64_t* dp_rows, uint64_t* flex_rows, uint64_t* rw_rows) {
+  return tsd::guarded([&] {
+    if (!t) tsd::fail(TS_ERR_CONFIG, "ts_table_shard_rows: null table");
+    if (dp_rows) *dp_rows = t->dp_rows;
+    if (flex_rows) *flex_rows = t->flex_rows;
+    if (rw_rows) *rw_rows = t->rw_rows;
+  });
+}
+
+ts_status ts_table_stream(ts_table* t, void** stream) {
+  return tsd::guarded([&] {
+    if (!t || !stream) tsd::fail(TS_ERR_CONFIG, "ts_table_stream: null argument");
+    *stream = static_cast<void*>(t->stream);
+  });
+}
+
+ts_status ts_table_forward(ts_table* t, const uint32_t* d_rows, uint64_t occ, float* d_out) {
+  return tsd::guarded([&] {
+    if (!t || (occ && (!d_rows || !d_out))) tsd::fail(TS_ERR_CONFIG, "ts_table_forward: null argument");
+    TSD_CUDA(cudaSetDevice(t->cfg.device));
+    t->forward(d_rows, occ, d_out);
+  });
+}
+
+ts_status ts_table_backward(ts_table* t, const float* d_grad) {
+  return tsd::guarded([&] {
+    if (!t || (t->last_occ && !d_grad)) tsd::fail(TS_ERR_CONFIG, "ts_table_backward: null argument");
+    TSD_CUDA(cudaSetDevice(t->cfg.device));
+    t->backward(d_grad);
+  });
+}
+
+ts_status ts_table_train_step(ts_table* t, const uint32_t* d_rows, uint64_t occ, float* d_out) {
+  return tsd::guarded([&] {
+    if (!t || (occ && (!d_rows || !d_out))) tsd::fail(TS_ERR_CONFIG, "ts_table_train_step: null argument");
+    TSD_CUDA(cudaSetDevice(t->cfg.device));
+    t->forward(d_rows, occ, d_out);
+    t->backward(d_out);  // loss = 0.5*|out|^2  =>  d loss / d out = out
+  });
+}
+
+ts_status ts_table_train_step_host(ts_table* t, const uint32_t* h_rows, uint64_t occ, double* h_loss) {
+  return tsd::guarded([&] {
+    if (!t || (occ && !h_rows)) tsd::fail(TS_ERR_CONFIG, "ts_table_train_step_host: null argument");
+    TSD_CUDA(cudaSetDevice(t->cfg.device));
+    t->rows_dev.ensure(std::max<uint64_t>(occ, 1));
+    static thread_local tsd::DevBuf<float> out;  // per-thread scratch output
+    if (occ) {
+      TSD_CUDA(cudaMemcpyAsync(t->rows_dev.ptr, h_rows, sizeof(uint32_t) * occ, cudaMemcpyHostToDevice,
+                               t->stream));
+    }
+    out.ensure(std::max<uint64_t>(occ, 1) * t->cfg.dim);
+    t->forward(t->rows_dev.ptr, occ, out.ptr);
+    t->backward(out.ptr);
+    double loss = 0.0;
+    TSD_CUDA(cudaMemcpyAsync(&loss, t->d_loss.ptr, sizeof(double), cudaMemcpyDeviceToHost, t->stream));
+    TSD_CUDA(cudaStreamSynchronize(t->stream));
+    if (h_loss) *h_loss = loss;
+  });
+}
+
+ts_status ts_table_loss(ts_table* t, double* loss) {
+  return tsd::guarded([&] {
+    if (!t || !loss) tsd::fail(TS_ERR_CONFIG, "ts_table_loss: null argument");
+    TSD_CUDA(cudaSetDevice(t->cfg.device));
+    TSD_CUDA(cudaMemcpyAsync(loss, t->d_loss.ptr, sizeof(double), cudaMemcpyDeviceToHost, t->stream));
+    TSD_CUDA(cudaStreamSynchronize(t->stream));
+  });
+}
+
+ts_status ts_table_counters(ts_table* t, uint64_t* counters) {
+  return tsd::guarded([&] {
+    if (!t || !counters) tsd::fail(TS_ERR_CONFIG, "ts_table_counters: null argument");
+    TSD_CUDA(cudaSetDevice(t->cfg.device));
+    const uint32_t U = t->U, g = t->g;
+    std::memset(counters, 0, sizeof(uint64_t) * TS_NUM_COUNTERS * U);
+    unsigned long long tiers[3] = {0, 0, 0};
+    uint32_t nseg = 0;
+    TSD_CUDA(cudaMemcpyAsync(tiers, t->tier_counts.ptr, sizeof(tiers), cudaMemcpyDeviceToHost, t->stream));
+    TSD_CUDA(cudaMemcpyAsync(&nseg, t->nseg.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, t->stream));
+    TSD_CUDA(cudaStreamSynchronize(t->stream));
+    if (U == 1) {
+      // tiers are not bucketed at U == 1; count them from the placement cuts
+      // on the device-less path: every occurrence is local.
+      std::vector<uint32_t> rows(t->last_occ);
+      if (t->last_occ) {
+        TSD_CUDA(cudaMemcpy(rows.data(), t->last_rows, sizeof(uint32_t) * t->last_occ,
+                            cudaMemcpyDeviceToHost));
+      }
+      for (const uint32_t c : rows) {
+        if (c < t->cfg.dp_cut) ++tiers[2];
+        else if (c < t->cfg.flex_cut) ++tiers[1];
+        else ++tiers[0];
+      }
+    }
+    // requester column g
+    counters[TS_CTR_RECV_GLOBAL * U + g] = tiers[0];
+    counters[TS_CTR_RECV_INTRA * U + g] = tiers[1];
+    counters[TS_CTR_DP_LOCAL * U + g] = tiers[2];
+    // server column g: every entry served here, by tier
+    uint64_t rw_served = 0, flex_served = 0;
+    if (U == 1) {
+      rw_served = tiers[0];
+      flex_served = tiers[1];
+    } else {
+      // local own-shard occurrences (RW owned by g / Flex in my slot) plus received ones
+      const uint32_t nb = t->nb();
+      auto start_of = [&](uint32_t p, uint32_t b) -> uint64_t {
+        return t->h_counts[size_t{p} * (nb + 1) + b];
+      };
+      for (uint32_t p = 0; p < U; ++p) {
+        if (p == g) continue;
+        rw_served += start_of(p, g + 1) - start_of(p, g);
+        if (p / t->W == t->node) flex_served += start_of(p, U + t->slot + 1) - start_of(p, U + t->slot);
+      }
+      // own RW/Flex occurrences served locally = my tiers minus what I sent
+      uint64_t rw_sent = 0, flex_sent = 0;
+      for (uint32_t b = 0; b < U; ++b) rw_sent += start_of(g, b + 1) - start_of(g, b);
+      for (uint32_t b = U; b < U + t->W; ++b) flex_sent += start_of(g, b + 1) - start_of(g, b);
+      rw_served += tiers[0] - rw_sent;
+      flex_served += tiers[1] - flex_sent;
+    }
+    counters[TS_CTR_SEND_GLOBAL * U + g] = rw_served;
+    counters[TS_CTR_SEND_INTRA * U + g] = flex_served;
+    counters[TS_CTR_SERVED * U + g] = t->last_entries;
+    counters[TS_CTR_DISTINCT * U + g] = nseg;
+  });
+}
+
+ts_status ts_table_read_rows(ts_table* t, const uint32_t* rows, uint64_t count, float* h_weights,
+                             float* h_state) {
+  return tsd::guarded([&] {
+    if (!t || (count && (!rows || !h_weights))) tsd::fail(TS_ERR_CONFIG, "ts_table_read_rows: null argument");
+    TSD_CUDA(cudaSetDevice(t->cfg.device));
+    TSD_CUDA(cudaStreamSynchronize(t->stream));
+    const uint32_t dim = t->cfg.dim;
+    for (uint64_t k = 0; k < count; ++k) {
+      const uint32_t c = rows[k];
+      if (c >= t->cfg.n_rows) tsd::fail(TS_ERR_VALIDATION, "read_rows: row outside the plan");
+      uint64_t lid = c;
+      if (t->U > 1 && c >= t->cfg.dp_cut) {
+        const uint8_t d = t->h_dest[c];
+        const bool mine = c < t->cfg.flex_cut ? d == t->slot : d == t->g;
+        if (!mine) tsd::fail(TS_ERR_VALIDATION, "read_rows: row is not stored on this rank");
+        lid = t->h_local[c];
+      }
+      TSD_CUDA(cudaMemcpy(h_weights + k * dim, t->d_w + lid * dim, sizeof(float) * dim,
+                          cudaMemcpyDeviceToHost));
+      if (h_state && t->d_state) {
+        TSD_CUDA(cudaMemcpy(h_state + k, t->d_state + lid, sizeof(float), cudaMemcpyDeviceToHost));
+      }
+    }
+  });
+}
+
+ts_status ts_table_synchronize(ts_table* t) {
+  return tsd::guarded([&] {
+    if (!t) tsd::fail(TS_ERR_CONFIG, "ts_table_synchronize: null table");
+    TSD_CUDA(cudaSetDevice(t->cfg.device));
+    TSD_CUDA(cudaStreamSynchronize(t->stream));
+  });
+}
+
+ts_status ts_table_enable_timing(ts_table* t, int enable) {
+  return tsd::guarded([&] {
+    if (!t) tsd::fail(TS_ERR_CONFIG, "ts_table_enable_timing: null table");
+    TSD_CUDA(cudaSetDevice(t->cfg.device));
+    t->collect_timing();
+    t->timing = enable != 0;
+    std::fill(std::begin(t->phase_ms), std::end(t->phase_ms), 0.0);
+    std::fill(std::begin(t->phase_launches), std::end(t->phase_launches), 0);
+  });
+}
+
+ts_status ts_table_phase_times(ts_table* t, double* ms, uint64_t* launches, int capacity, int* count) {
+  return tsd::guarded([&] {
+    if (!t) tsd::fail(TS_ERR_CONFIG, "ts_table_phase_times: null table");
+    TSD_CUDA(cudaSetDevice(t->cfg.device));
+    t->collect_timing();
+    const int n = std::min<int>(capacity, tsd::kNumPhases);
+    for (int i = 0; i < n; ++i) {
+      if (ms) ms[i] = t->phase_ms[i];
+      if (launches) launches[i] = t->phase_launches[i];
+    }
+    if (count) *count = tsd::kNumPhases;
+  });
+}
+
+const char* ts_table_phase_name(int phase) {
+  return phase >= 0 && phase < tsd::kNumPhases ? tsd::kPhaseNames[phase] : "?";
+}
+
+}  // extern "C"

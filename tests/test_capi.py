@@ -1,0 +1,55 @@
+"""The drop-in boundary: libtiershard_b200.so loads, exports every entry point
+include/tiershard_b200.h declares, and fails loudly (no CPU fallback) where
+no device is present."""
+import re
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2301_02959_b200 as ts
+from paper_2301_02959_b200 import capi
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_symbols():
+    text = (ROOT / "include" / "tiershard_b200.h").read_text()
+    return sorted(set(re.findall(r"\b(ts_[a-z_]+)\s*\(", text)))
+
+
+def test_header_and_binding_agree():
+    assert sorted(capi.EXPORTS) == declared_symbols()
+
+
+def test_library_exports_every_symbol():
+    out = subprocess.run(["nm", "-D", "--defined-only", str(capi.LIB_PATH)], capture_output=True,
+                         text=True, check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if line.strip()}
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+    lib = ts.load()
+    for s in declared_symbols():
+        assert hasattr(lib, s)
+    assert lib.ts_abi_version() == 1
+    assert "sm_100a" in ts.build_info()
+
+
+def test_no_cpu_fallback_without_device():
+    if ts.device_count() > 0:
+        pytest.skip("a device is present")
+    with pytest.raises(ts.TSError) as e:
+        ts.Table(n_rows=10, dim=32, dp_cut=0, flex_cut=0)
+    assert e.value.kind == "NoDevice"
+    with pytest.raises(ts.TSError) as e:
+        ts.Router(10, 0, 0, np.zeros(10, np.uint8), 1, 1)
+    assert e.value.kind == "NoDevice"
+    assert "no CPU fallback" in e.value.message
+
+
+def test_config_errors_before_device():
+    with pytest.raises(ts.TSError) as e:
+        ts.Router(10, 5, 2, np.zeros(10, np.uint8), 1, 1)
+    assert e.value.kind == "ValidationError"
+    assert "plan does not cover" in e.value.message
