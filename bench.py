@@ -1,0 +1,526 @@
+#!/usr/bin/env python
+"""bench.py — FlexShard per-row tiered sequence embedding, forward + backward.
+
+One step = one training step of the tiered sequence-embedding path on one
+batch: route -> (exchange) -> unpooled L x D gather -> loss 0.5*|out|^2 ->
+backward (reverse exchange, dedup sort, segment-reduce, DP/Flex all-reduce)
+-> fused row-wise Adagrad, all through the C-ABI of libtiershard_b200.so.
+
+Workload (BASELINE.json configs[1], "C2"): 8 tables x 10M rows x D=128 fp32,
+seq len 128 per table (L_total = 1024), batch 4096 per GPU, Zipf 1.05,
+synthesized with the reference's synthesize_zipf (seeds 1000+t) and sampled
+with its Workload (seed 7) by the product's bit-exact host API (ts_driver).
+Rows are sharded over N GPUs (topology 1 x N, homogeneous NVSwitch =>
+2-tier plan; --virtual-nodes uses 2 x N/2 with the paper's bandwidths and a
+3-tier plan).  Per-GPU batch fixed => "scaling": "weak".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun each rank drives its own GPU; timing is CUDA events on the
+table's stream, summed over the K timed steps (L2 flushed between steps
+outside the events), max over ranks.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "sequence samples/sec fwd+bwd (8×B200) + all-to-all GB saved vs row-wise; HBM GB/s"
+HOMO = dict(a2a_global_gibs=1, a2a_intra_gibs=1, ar_global_gibs=1, ar_cross_gibs=1)
+PAPER_BW = dict(a2a_global_gibs=23, a2a_intra_gibs=95, ar_global_gibs=73, ar_cross_gibs=15)
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--tables", type=int, default=8)
+    p.add_argument("--rows", type=int, default=10_000_000)
+    p.add_argument("--dim", type=int, default=128)
+    p.add_argument("--seq-len", type=int, default=128, help="expected occurrences per table per sample")
+    p.add_argument("--batch", type=int, default=4096, help="samples per GPU")
+    p.add_argument("--exponent", type=float, default=1.05)
+    p.add_argument("--iterations", type=int, default=4, help="distinct batches cycled by the timed loop")
+    p.add_argument("--optimizer", choices=("sgd", "adagrad"), default="adagrad")
+    p.add_argument("--lr", type=float, default=0.01)
+    p.add_argument("--virtual-nodes", action="store_true", help="2 x N/2 virtual nodes, paper bw, 3-tier")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cache", default="/tmp/tiershard_bench")
+    return p.parse_args()
+
+
+# --------------------------------------------------------------------------
+# distributed plumbing (gloo on the host: barrier, max, id broadcast)
+# --------------------------------------------------------------------------
+
+class Dist:
+    def __init__(self):
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as td
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            td.init_process_group("gloo", rank=self.rank, world_size=self.world)
+            self.td = td
+
+    def barrier(self):
+        if self.world > 1:
+            self.td.barrier()
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64)
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64)
+        self.td.all_reduce(t, op=self.td.ReduceOp.SUM)
+        return float(t.item())
+
+    def bcast(self, obj):
+        if self.world == 1:
+            return obj
+        box = [obj]
+        self.td.broadcast_object_list(box, src=0)
+        return box[0]
+
+    def close(self):
+        if self.world > 1:
+            self.td.destroy_process_group()
+
+
+# --------------------------------------------------------------------------
+# workload preparation (host C++ planner via ts_driver, cached on disk)
+# --------------------------------------------------------------------------
+
+def workload_spec(args, n_gpus):
+    if args.virtual_nodes and n_gpus >= 4 and n_gpus % 2 == 0:
+        topo = dict(num_nodes=2, gpus_per_node=n_gpus // 2, **PAPER_BW)
+        goal = "3tier"
+    else:
+        topo = dict(num_nodes=1, gpus_per_node=n_gpus, **HOMO)
+        goal = "2tier"
+    tables = [dict(table_id=t, rows=args.rows, exponent=args.exponent, target_length=args.seq_len,
+                   seed=1000 + t) for t in range(args.tables)]
+    return dict(tables=tables, topology=topo,
+                cost_model=dict(local_batch=args.batch, embedding_dim=args.dim), goal=goal,
+                frontier=False, hash_seed=2, workload=dict(seed=7, iterations=args.iterations))
+
+
+def prepare(args, dist: Dist, n_gpus):
+    from paper_2301_02959_b200 import DRIVER_PATH
+    spec = workload_spec(args, n_gpus)
+    key = hashlib.sha1(json.dumps(spec, sort_keys=True).encode()).hexdigest()[:16]
+    out_dir = Path(args.cache) / key
+    meta_path = out_dir / "meta.json"
+    if dist.rank == 0 and not meta_path.exists():
+        out_dir.mkdir(parents=True, exist_ok=True)
+        spec_run = dict(spec, export_dir=str(out_dir))
+        (out_dir / "spec.json").write_text(json.dumps(spec_run))
+        t0 = time.time()
+        subprocess.run([str(DRIVER_PATH), str(out_dir / "spec.json"), str(out_dir / "doc.json")],
+                       check=True)
+        doc = json.loads((out_dir / "doc.json").read_text())
+        if "error" in doc:
+            raise RuntimeError(doc)
+        doc["prep_wall_s"] = time.time() - t0
+        meta_path.write_text(json.dumps(doc))
+    dist.barrier()
+    doc = json.loads(meta_path.read_text())
+    return spec, out_dir, doc
+
+
+# --------------------------------------------------------------------------
+# clocks sampling during the timed region
+# --------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(self.NAMES, parts[2:6]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        under_load = [s for s in sm if s > 0.5 * max(smax or [1])] or sm
+        return {"sm_mhz": float(np.median(under_load)) if under_load else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+
+PHASE_BYTES_DOC = {
+    "gather": "occ_local x (2*row_bytes + 4): index read, row read, row write",
+    "segment_update": "entries x (row_bytes + 8) + unique x (2*row_bytes + 8): grad + sorted pair read, "
+                      "weight read+write, Adagrad state read+write",
+    "dedup_sort": "passes x entries x 20: key read (histogram) + pair read + pair write",
+}
+
+
+def measured_peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+def run_ours(args, dist: Dist):
+    import torch
+    import paper_2301_02959_b200 as ts
+
+    n_gpus = dist.world if dist.world > 1 else args.gpus
+    if dist.world == 1 and n_gpus > 1:
+        raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    spec, data_dir, doc = prepare(args, dist, n_gpus)
+    exp = doc["export"]
+    u, w = exp["num_gpus"], exp["gpus_per_node"]
+    B, D = exp["local_batch"], exp["embedding_dim"]
+    g = dist.rank
+    device = dist.local_rank
+    torch.cuda.set_device(device)
+    plan = doc["plan"]
+    dest = np.fromfile(data_dir / "dest.u8", np.uint8)
+    batches = []
+    for it in range(exp["iterations"]):
+        rows = np.fromfile(data_dir / f"batch_{it}.rows.u32", np.uint32)
+        off = np.fromfile(data_dir / f"batch_{it}.offsets.u64", np.uint64)
+        lo, hi = int(off[g * B]), int(off[(g + 1) * B])
+        batches.append(np.ascontiguousarray(rows[lo:hi]))
+    max_occ = max(b.size for b in batches)
+
+    nccl_id = None
+    if u > 1:
+        nccl_id = dist.bcast(ts.nccl_unique_id() if g == 0 else None)
+    opt = ts.OPT_ROWWISE_ADAGRAD if args.optimizer == "adagrad" else ts.OPT_SGD
+    table = ts.Table(n_rows=exp["n_rows"], dim=D, dp_cut=plan["dp_cut"], flex_cut=plan["flex_cut"],
+                     tier_dest=dest if u > 1 else None, num_nodes=u // w, gpus_per_node=w, rank=g,
+                     device=device, weight_seed=1234, optimizer=opt, lr=args.lr,
+                     max_occurrences=max_occ, nccl_unique_id=nccl_id)
+    stream = torch.cuda.ExternalStream(table.stream(), device=device)
+    d_rows = [torch.from_numpy(b.view(np.int32)).to(f"cuda:{device}") for b in batches]
+    d_out = torch.empty((max_occ, D), dtype=torch.float32, device=f"cuda:{device}")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{device}")  # 2x L2
+    torch.cuda.synchronize()
+
+    def step(k):
+        b = d_rows[k % len(d_rows)]
+        table.train_step(b.data_ptr(), b.numel(), d_out.data_ptr())
+
+    for k in range(args.warmup):
+        step(k)
+    table.synchronize()
+    dist.barrier()
+
+    # ---- timed region: device-side, CUDA events on the table stream --------
+    clocks = ClockSampler(device)
+    clocks.start()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = ts.kernel_launches()
+    table.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier()
+    wall0 = time.perf_counter()
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()  # evict L2 (outside the timed events)
+            starts[k].record(stream)
+        step(args.warmup + k)
+        with torch.cuda.stream(stream):
+            ends[k].record(stream)
+    table.synchronize()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    launches = ts.kernel_launches() - launches0
+    dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    dev_ms = dist.max(dev_ms)
+    samples = u * B * args.steps
+    value = samples / (dev_ms / 1e3)
+    loss = table.loss()
+    counters = table.counters()
+
+    # ---- per-phase device times (roofline numerator) ------------------------
+    table.enable_timing(True)
+    prof_steps = min(args.steps, 20)
+    for k in range(prof_steps):
+        step(k)
+    phases = table.phase_times()
+    table.enable_timing(False)
+    clk = clocks.stop()
+
+    # ---- end to end through the host-buffer public entry point -------------
+    e2e = None
+    if not args.no_e2e:
+        pinned = [torch.from_numpy(b.view(np.int32)).pin_memory().numpy().view(np.uint32) for b in batches]
+        for k in range(min(args.warmup, 3)):
+            table.train_step_host(pinned[k % len(pinned)])
+        dist.barrier()
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            table.train_step_host(pinned[k % len(pinned)])
+        e2e_s = dist.max(time.perf_counter() - t0)
+        h2d = float(np.mean([pinned[k % len(pinned)].nbytes for k in range(args.steps)]))
+        e2e = {"value": samples / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": 8}
+
+    # ---- roofline of the dominant kernel -----------------------------------
+    row_bytes = D * 4
+    occ_mean = float(np.mean([b.size for b in batches]))
+    distinct = float(counters[6, g])
+    entries = float(counters[5, g])
+    n_local_occ = occ_mean if u == 1 else float(counters[4, g] + counters[0, g] + counters[2, g])
+    key_bits = int(np.ceil(np.log2(max(2, exp["n_rows"] if u == 1 else exp["n_rows"] // u))))
+    passes = (key_bits + 7) // 8
+    algo = {
+        "gather": n_local_occ * (2 * row_bytes + 4),
+        "segment_update": entries * (row_bytes + 8) + distinct * (2 * row_bytes + (8 if opt else 0)),
+        "dedup_sort": passes * entries * 20,
+    }
+    per_launch_ms = {k: (v[0] / max(1, v[1])) for k, v in phases.items() if v[1]}
+    dominant = max((k for k in algo if k in per_launch_ms), key=lambda k: per_launch_ms[k])
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = algo[dominant] / (per_launch_ms[dominant] / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dominant, "achieved": round(achieved, 1),
+                "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
+                "algorithmic_bytes_per_launch": algo[dominant], "avg_launch_ms": per_launch_ms[dominant],
+                "bytes_model": PHASE_BYTES_DOC[dominant],
+                "all_phases_ms_per_step": {k: round(v[0] / max(1, v[1]), 4) for k, v in phases.items() if v[1]}}
+    for k in ("gather", "segment_update"):
+        if k in per_launch_ms:
+            roofline[f"{k}_gbs"] = round(algo[k] / (per_launch_ms[k] / 1e3) / 1e9, 1)
+
+    # ---- all-to-all bytes saved (plan vs RW vs TW, per iteration, whole job) --
+    tr = exp["traffic"]
+    ref_conv = {k: float(np.mean([t["reference_convention"][k] for t in tr]))
+                for k in tr[0]["reference_convention"]}
+    off_dev = {k: float(np.mean([t["off_device"][k] for t in tr])) for k in tr[0]["off_device"]}
+    a2a = {
+        "unit": "GB per iteration (one direction, one pass, whole job)",
+        "saved_vs_rw_reference_convention": (ref_conv["rw_global_bytes"] - ref_conv["plan_global_bytes"]) / 1e9,
+        "saved_vs_tw_reference_convention": (ref_conv["tw_global_bytes"] - ref_conv["plan_global_bytes"]) / 1e9,
+        "global_a2a_reduction": 1 - ref_conv["plan_global_bytes"] / ref_conv["rw_global_bytes"],
+        "predicted_reduction": plan["predicted"]["global_a2a_reduction"],
+        "saved_vs_rw_off_device": (off_dev["rw_bytes"] - off_dev["plan_global_bytes"] - off_dev["plan_intra_bytes"]) / 1e9,
+        "saved_vs_tw_off_device": (off_dev["tw_bytes"] - off_dev["plan_global_bytes"] - off_dev["plan_intra_bytes"]) / 1e9,
+        "plan_off_device_GB": (off_dev["plan_global_bytes"] + off_dev["plan_intra_bytes"]) / 1e9,
+    }
+
+    cpu = None
+    if dist.rank == 0 and u == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_port(batches[0], dest, plan, exp, B, D, args)
+
+    result = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "samples/s",
+        "n_gpus": u,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(dev_ms / args.steps, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic: reference synthesize_zipf (seeds 1000+t) + Workload (seed 7), materialized "
+                "bit-exactly by the product host API; weights seeded-hash init",
+        "config": {
+            "workload": f"C2: {args.tables} tables x {args.rows} rows x D={D} fp32, seq len {args.seq_len}"
+                        f"/table, batch {B}/GPU, Zipf {args.exponent}",
+            "topology": f"{u // w} x {w}" + (" virtual nodes, paper bw" if args.virtual_nodes else " homogeneous"),
+            "plan": plan["goal"], "dp_cut": plan["dp_cut"], "flex_cut": plan["flex_cut"],
+            "global_batch": u * B, "seq_len": args.seq_len * args.tables,
+            "parallelism": f"row-sharded over {u} GPU(s): DP/Flex/RW tiers",
+            "optimizer": args.optimizer, "l2": "flushed (256 MiB write) between timed steps, outside events",
+            "batches_cycled": len(batches), "occurrences_per_gpu_step": occ_mean,
+        },
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "roofline": roofline,
+        "a2a": a2a,
+        "loss_last_step": loss,
+        "wall_s_timed": round(wall, 4),
+        "prep_wall_s": doc.get("prep_wall_s"),
+    }
+    if cpu is not None:
+        result["cpu_baseline"] = cpu
+    table.close()
+    return result
+
+
+def cpu_baseline_port(rows, dest, plan, exp, B, D, args):
+    """Oracle port (oracle/restate.c) of one step on the host cores: the
+    reference's routing loop restated (single thread, as the reference runs
+    one iteration) + gather + dedup/segment-sum + row-wise Adagrad (threaded).
+    Bounded sample: the first batch of the workload, weights compacted to the
+    rows it touches (same values: seeded by canonical index)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_bind as orc
+    n = exp["n_rows"]
+    threads = len(os.sched_getaffinity(0))
+    dp, fx = plan["dp_cut"], plan["flex_cut"]
+    idx = np.arange(n, dtype=np.uint64)
+    tier = np.where(idx < dp, 0, np.where(idx < fx, 1, 2)).astype(np.uint8)
+    owner = np.where(tier == 2, dest, 0).astype(np.uint32)
+    slot = np.where(tier == 1, dest, 0).astype(np.uint32)
+    del idx
+    off = np.array([0, rows.size], np.uint64)
+    t0 = time.perf_counter()
+    orc.route_counts(1, 1, 1, off, rows, tier, owner, slot)
+    t_route = time.perf_counter() - t0
+    uniq, compact = np.unique(rows, return_inverse=True)
+    w = orc.init_rows(1234, uniq.astype(np.uint32), D, threads)
+    state = np.zeros(uniq.size, np.float32)
+    compact = compact.astype(np.uint32)
+    t0 = time.perf_counter()
+    out = orc.gather(w, compact, threads)
+    orc.backward_update(w, state, compact, out, orc.OPT_ROWWISE_ADAGRAD, args.lr, 1e-8, threads)
+    t_value = time.perf_counter() - t0
+    total = t_route + t_value
+    return {"value": round(B / total, 2), "unit": "samples/s", "cores": threads, "kind": "port",
+            "sample": f"one C2 batch ({B} samples, {rows.size} occurrences): restated reference routing "
+                      f"loop {t_route:.3f}s (1 thread) + gather/dedup/Adagrad {t_value:.3f}s "
+                      f"({threads} threads); weights compacted to the {uniq.size} touched rows"}
+
+
+# --------------------------------------------------------------------------
+# reference arm: the reference's own CPU path (oracle/_ref, unmodified)
+# --------------------------------------------------------------------------
+
+def run_reference(args, dist: Dist):
+    n_gpus = dist.world if dist.world > 1 else args.gpus
+    if dist.rank != 0:
+        return None
+    ref = ROOT / "oracle" / "_ref" / "ref_driver"
+    if not ref.exists():
+        return {"impl": "reference", "unavailable": "oracle/_ref/ref_driver was not built (needs /root/reference)"}
+    spec = workload_spec(args, n_gpus)
+    threads = max(1, min(len(os.sched_getaffinity(0)), args.steps, 32))
+    spec["workload"] = dict(seed=7, iterations=args.steps, materialize_pass=False)
+    spec["threads"] = threads
+    spec["simulate"] = True
+    spec["frontier"] = False
+    tmp = Path(args.cache) / "reference"
+    tmp.mkdir(parents=True, exist_ok=True)
+    (tmp / "spec.json").write_text(json.dumps(spec))
+    t0 = time.time()
+    subprocess.run([str(ref), str(tmp / "spec.json"), str(tmp / "out.json")], check=True)
+    doc = json.loads((tmp / "out.json").read_text())
+    wall = time.time() - t0
+    sim_s = doc["timing"]["simulate_s"]
+    u = spec["topology"]["num_nodes"] * spec["topology"]["gpus_per_node"]
+    samples = args.steps * u * args.batch
+    value = samples / sim_s
+    return {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "samples/s",
+        "n_gpus": n_gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(1e3 * sim_s / args.steps, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64 (integer routing + fp64 accounting)",
+        "data": "synthetic (same workload as --impl ours)",
+        "config": {"workload": f"C2: {args.tables} tables x {args.rows} rows x D={args.dim}, seq len "
+                               f"{args.seq_len}/table, batch {args.batch}/GPU, Zipf {args.exponent}",
+                   "topology": f"{spec['topology']['num_nodes']} x {spec['topology']['gpus_per_node']}",
+                   "plan": spec["goal"]},
+        "cpu_baseline": {"value": round(value, 2), "unit": "samples/s", "cores": threads, "kind": "reference",
+                         "sample": f"tiershard::simulate (unmodified reference, oracle/_ref) over {args.steps} "
+                                   f"iterations of the workload, threads={threads}: its stock path samples each "
+                                   "iteration and routes/counts every occurrence; the reference has no "
+                                   "gather/exchange/update to time"},
+        "e2e": {"value": round(value, 2), "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_timing": doc["timing"],
+        "wall_s": round(wall, 1),
+        "global_a2a_reduction": doc.get("comparison", {}).get("global_a2a_reduction"),
+    }
+
+
+def main():
+    args = parse_args()
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            res = run_reference(args, dist)
+        else:
+            res = run_ours(args, dist)
+        if dist.rank == 0 and res is not None:
+            print(json.dumps(res), flush=True)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -74,6 +74,12 @@ const char* ts_build_info(void);
 int ts_abi_version(void);
 /* Number of CUDA devices visible (0 when no driver/device). */
 ts_status ts_device_count(int* count);
+/* A fresh 128-byte ncclUniqueId (rank 0 creates it and broadcasts it to the
+ * other ranks through any host channel before ts_table_create). */
+ts_status ts_nccl_unique_id(void* out128);
+/* Number of device kernels this library has launched in this process (the
+ * bench's gpu_launches evidence). */
+uint64_t ts_kernel_launches(void);
 
 /* ------------------------------------------------------------------------
  * Router: the reference's routing + traffic-accounting loop on one GPU for a

@@ -292,7 +292,7 @@ json run(const json& spec) {
   const ts::Workload wl = ts::sample_workload(dist, cfg, topo, wseed, iters);
   timing["workload_build_s"] = now_s() - t0;
 
-  {
+  if (jw.value("materialize_pass", true)) {
     ts::IterationBatch batch;
     json occ = json::array();
     t0 = now_s();

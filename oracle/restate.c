@@ -266,6 +266,27 @@ void orc_init_table(uint64_t seed, uint64_t n, uint32_t dim, float* w, int threa
 }
 
 typedef struct {
+  uint64_t seed, count;
+  uint32_t dim;
+  const uint32_t* canon;
+  float* w;
+} init_rows_args;
+
+static void init_rows_job(int tid, int nt, void* p) {
+  init_rows_args* a = (init_rows_args*)p;
+  const uint64_t lo = a->count * tid / nt, hi = a->count * (tid + 1) / nt;
+  for (uint64_t k = lo; k < hi; ++k)
+    for (uint32_t d = 0; d < a->dim; ++d)
+      a->w[k * a->dim + d] = orc_init_weight(a->seed, a->canon[k], d, a->dim);
+}
+
+void orc_init_rows(uint64_t seed, const uint32_t* canon, uint64_t count, uint32_t dim,
+                   float* w, int threads) {
+  init_rows_args a = {seed, count, dim, canon, w};
+  run_par(init_rows_job, &a, threads);
+}
+
+typedef struct {
   const float* w;
   uint32_t dim;
   const uint32_t* rows;

@@ -78,6 +78,9 @@ int orc_iteration_metrics(uint32_t num_gpus, uint32_t embedding_dim,
  *   w = (float)v * 2^-23 * 0.01   (exact in fp32, |w| <= 0.01)            */
 float orc_init_weight(uint64_t seed, uint64_t c, uint32_t d, uint32_t dim);
 void orc_init_table(uint64_t seed, uint64_t n, uint32_t dim, float* w, int threads);
+/* w[k,:] = initial weights of canonical row canon[k] (compact tables). */
+void orc_init_rows(uint64_t seed, const uint32_t* canon, uint64_t count, uint32_t dim,
+                   float* w, int threads);
 
 /* Unpooled sequence gather: out[i,:] = w[rows[i],:]. */
 void orc_gather(const float* w, uint32_t dim, const uint32_t* rows, uint64_t occ,

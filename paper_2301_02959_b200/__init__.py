@@ -15,6 +15,8 @@ from .capi import (  # noqa: F401
     load,
     build_info,
     device_count,
+    nccl_unique_id,
+    kernel_launches,
     COUNTER_NAMES,
     OPT_SGD,
     OPT_ROWWISE_ADAGRAD,

@@ -44,6 +44,8 @@ EXPORTS = (
     "ts_build_info",
     "ts_abi_version",
     "ts_device_count",
+    "ts_nccl_unique_id",
+    "ts_kernel_launches",
     "ts_router_create",
     "ts_router_iteration",
     "ts_router_iteration_device",
@@ -118,6 +120,8 @@ def load() -> C.CDLL:
         "ts_build_info": (C.c_char_p, []),
         "ts_abi_version": (C.c_int, []),
         "ts_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+        "ts_nccl_unique_id": (C.c_int, [vp]),
+        "ts_kernel_launches": (C.c_uint64, []),
         "ts_router_create": (C.c_int, [C.POINTER(vp), C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
                                        vp, C.c_uint32, C.c_uint32]),
         "ts_router_iteration": (C.c_int, [vp, C.c_uint32, vp, vp, C.c_uint64, vp]),
@@ -165,6 +169,16 @@ def device_count() -> int:
     n = C.c_int(0)
     _check(load().ts_device_count(C.byref(n)))
     return n.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(load().ts_nccl_unique_id(buf))
+    return buf.raw
+
+
+def kernel_launches() -> int:
+    return int(load().ts_kernel_launches())
 
 
 class Router:

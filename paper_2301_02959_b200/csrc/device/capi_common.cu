@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <atomic>
+#include <cstring>
 #include <string>
 
 #include "common.cuh"
@@ -11,9 +13,12 @@ namespace tsd {
 
 namespace {
 thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
 }
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void use_device(int device) {
   int count = 0;
@@ -73,5 +78,20 @@ ts_status ts_device_count(int* count) {
     *count = n;
   });
 }
+
+ts_status ts_nccl_unique_id(void* out128) {
+  return tsd::guarded([&] {
+    if (!out128) tsd::fail(TS_ERR_CONFIG, "ts_nccl_unique_id: null output");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) {
+      tsd::fail(TS_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    }
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+uint64_t ts_kernel_launches(void) { return tsd::g_launches.load(std::memory_order_relaxed); }
 
 }  // extern "C"

@@ -32,8 +32,15 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
   }
 }
 
+// Counts every kernel launch of the library (ts_kernel_launches()).
+void note_launch();
+
 #define TSD_CUDA(call) ::tsd::cuda_check((call), #call, __FILE__, __LINE__)
-#define TSD_LAUNCH_CHECK() ::tsd::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+#define TSD_LAUNCH_CHECK()                                                   \
+  do {                                                                       \
+    ::tsd::note_launch();                                                    \
+    ::tsd::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__); \
+  } while (0)
 
 // Selects `device` after verifying it exists and is an sm_100-class part.
 void use_device(int device);

@@ -13,7 +13,9 @@
 #include <iostream>
 #include <memory>
 #include <string>
+#include <algorithm>
 #include <thread>
+#include <vector>
 
 #include "json.hpp"
 #include "tiershard/cost_model.hpp"
@@ -131,6 +133,71 @@ uint64_t digest_placements(const std::vector<ts::RowPlacement>& p) {
   return h;
 }
 
+template <typename T>
+void write_binary(const std::string& path, const std::vector<T>& v) {
+  std::ofstream f(path, std::ios::binary);
+  if (!f) throw ts::ConfigError("ts_driver: cannot write " + path);
+  f.write(reinterpret_cast<const char*>(v.data()), static_cast<std::streamsize>(v.size() * sizeof(T)));
+}
+
+// All-to-all bytes of one iteration under three shardings of the same rows:
+// the plan, pure row-wise (owner = h % U) and table-wise (owner = table % U,
+// builder-defined: the reference has no TW strategy).
+// "reference convention" counts every non-replicated occurrence (self sends
+// included, simulator.cpp:234-243); "off_device" counts only occurrences whose
+// server is another GPU — the bytes that actually cross NVLink.  One
+// direction, one pass, embedding payload only.
+Json traffic_json(const ts::IterationBatch& b, const ts::RowDistribution& d,
+                  const std::vector<ts::RowPlacement>& pl, uint32_t u, uint32_t w,
+                  const ts::CostModelConfig& cfg, uint64_t hash_seed) {
+  const double row_bytes = static_cast<double>(cfg.embedding_dim) * cfg.scalar_bytes;
+  uint64_t plan_global = 0, plan_intra = 0, plan_global_off = 0, plan_intra_off = 0;
+  uint64_t rw_off = 0, tw_off = 0, total = 0;
+  std::vector<uint64_t> rw_send(u, 0), tw_send(u, 0), plan_send(u, 0);
+  for (uint32_t g = 0; g < u; ++g) {
+    const uint64_t lo = b.sample_offsets[uint64_t{g} * b.local_batch];
+    const uint64_t hi = b.sample_offsets[uint64_t{g + 1} * b.local_batch];
+    const uint32_t node_base = (g / w) * w;
+    for (uint64_t k = lo; k < hi; ++k) {
+      const uint32_t r = b.rows[k];
+      const ts::RowRecord& rec = d.rows()[r];
+      ++total;
+      const uint32_t rw_owner = static_cast<uint32_t>(ts::row_key_hash(rec.table_id, rec.row_id, hash_seed) % u);
+      const uint32_t tw_owner = rec.table_id % u;
+      rw_off += rw_owner != g;
+      tw_off += tw_owner != g;
+      ++rw_send[rw_owner];
+      ++tw_send[tw_owner];
+      const ts::RowPlacement& p = pl[r];
+      if (p.tier == ts::Tier::kRowWise) {
+        ++plan_global;
+        plan_global_off += p.owner_gpu != g;
+        ++plan_send[p.owner_gpu];
+      } else if (p.tier == ts::Tier::kFlex) {
+        ++plan_intra;
+        plan_intra_off += node_base + p.flex_slot != g;
+      }
+    }
+  }
+  auto maxv = [](const std::vector<uint64_t>& v) { return *std::max_element(v.begin(), v.end()); };
+  return Json{{"occurrences", total},
+              {"row_bytes", row_bytes},
+              {"reference_convention",
+               {{"plan_global_bytes", plan_global * row_bytes},
+                {"plan_intra_bytes", plan_intra * row_bytes},
+                {"rw_global_bytes", total * row_bytes},
+                {"tw_global_bytes", total * row_bytes}}},
+              {"off_device",
+               {{"plan_global_bytes", plan_global_off * row_bytes},
+                {"plan_intra_bytes", plan_intra_off * row_bytes},
+                {"rw_bytes", rw_off * row_bytes},
+                {"tw_bytes", tw_off * row_bytes}}},
+              {"max_send_bytes",
+               {{"plan", maxv(plan_send) * row_bytes},
+                {"rw", maxv(rw_send) * row_bytes},
+                {"tw", maxv(tw_send) * row_bytes}}}};
+}
+
 Json run(const Json& spec) {
   Json out;
   Json timing;
@@ -234,7 +301,46 @@ Json run(const Json& spec) {
   const auto placements = ts::assign_rows(plan, d, topo, hash_seed);
   out["placements_digest"] = digest_placements(placements);
 
-  if (!spec.contains("workload")) {
+  if (spec.contains("export_dir")) {
+    // Bench/test preparation: the device remap bytes the planner emits, the
+    // cuts, and materialized batches — everything bench.py needs to drive
+    // the C-ABI without re-implementing the host API in Python.
+    t0 = seconds_now();
+    const std::string dir = spec["export_dir"].get<std::string>();
+    std::vector<uint8_t> dest(placements.size());
+    for (size_t i = 0; i < placements.size(); ++i) {
+      dest[i] = static_cast<uint8_t>(placements[i].tier == ts::Tier::kFlex ? placements[i].flex_slot
+                                                                          : placements[i].owner_gpu);
+    }
+    write_binary(dir + "/dest.u8", dest);
+    const Json& jw = spec.at("workload");
+    const uint32_t iters = jw.value("iterations", 1u);
+    const ts::Workload wl = ts::sample_workload(dist, cfg, topo, jw.value("seed", uint64_t{7}), iters);
+    std::vector<ts::IterationBatch> batches(iters);
+    {
+      std::vector<std::thread> pool;
+      for (uint32_t it = 0; it < iters; ++it) {
+        pool.emplace_back([&, it] { wl.materialize_iteration(it, batches[it]); });
+      }
+      for (auto& th : pool) th.join();
+    }
+    Json occ = Json::array();
+    Json traffic = Json::array();
+    const uint32_t u = topo.total_gpus(), w = topo.gpus_per_node;
+    for (uint32_t it = 0; it < iters; ++it) {
+      const auto& b = batches[it];
+      write_binary(dir + "/batch_" + std::to_string(it) + ".rows.u32", b.rows);
+      write_binary(dir + "/batch_" + std::to_string(it) + ".offsets.u64", b.sample_offsets);
+      occ.push_back(b.occurrences());
+      traffic.push_back(traffic_json(b, d, placements, u, w, cfg, hash_seed));
+    }
+    out["export"] = {{"dir", dir}, {"iterations", iters}, {"occurrences", occ}, {"traffic", traffic},
+                     {"n_rows", d.rows().size()}, {"num_gpus", u}, {"gpus_per_node", w},
+                     {"local_batch", cfg.local_batch}, {"embedding_dim", cfg.embedding_dim}};
+    timing["export_s"] = seconds_now() - t0;
+  }
+
+  if (!spec.contains("workload") || spec.contains("export_dir")) {
     out["timing"] = timing;
     return out;
   }

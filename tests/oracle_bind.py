@@ -49,6 +49,8 @@ def lib() -> C.CDLL:
         L.orc_init_weight.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32]
         L.orc_init_table.restype = None
         L.orc_init_table.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, vp, C.c_int]
+        L.orc_init_rows.restype = None
+        L.orc_init_rows.argtypes = [C.c_uint64, vp, C.c_uint64, C.c_uint32, vp, C.c_int]
         L.orc_gather.restype = None
         L.orc_gather.argtypes = [vp, C.c_uint32, vp, C.c_uint64, vp, C.c_int]
         L.orc_half_sq_sum.restype = C.c_double
@@ -115,6 +117,13 @@ def iteration_metrics(counters, *, dim, scalar_bytes=4, dyn=2, stat=1, include_i
 def init_table(seed, n, dim, threads=8):
     w = np.zeros((n, dim), np.float32)
     lib().orc_init_table(seed, n, dim, _p(w), threads)
+    return w
+
+
+def init_rows(seed, canon, dim, threads=8):
+    canon = np.ascontiguousarray(canon, dtype=np.uint32)
+    w = np.zeros((canon.size, dim), np.float32)
+    lib().orc_init_rows(seed, _p(canon), canon.size, dim, _p(w), threads)
     return w
 
 
