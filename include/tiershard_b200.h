@@ -113,6 +113,34 @@ ts_status ts_router_iteration_device(ts_router* r, const uint64_t* d_requester_b
 ts_status ts_router_destroy(ts_router* r);
 
 /* ------------------------------------------------------------------------
+ * Host-only planning helpers of the U > 1 path (no device needed).
+ * ---------------------------------------------------------------------- */
+
+/* Shard layout of rank g: local_id[i] for every canonical row i (the row's
+ * position inside the shard of the rank that serves it: DP rows keep i, Flex
+ * rows follow as [dp_cut + rank among rows of the same slot], RW rows as
+ * [dp_cut + flex rows of the owner's slot + rank among rows of the same
+ * owner]).  *dp_rows / *flex_rows / *rw_rows describe rank g's shard.
+ * local_id may be NULL. */
+ts_status ts_shard_layout(uint64_t n_rows, uint64_t dp_cut, uint64_t flex_cut,
+                          const uint8_t* tier_dest, uint32_t num_nodes,
+                          uint32_t gpus_per_node, uint32_t rank, uint32_t* local_id,
+                          uint64_t* dp_rows, uint64_t* flex_rows, uint64_t* rw_rows);
+
+/* All-to-allv plan of rank g from every rank's bucket starts (the counts the
+ * table all-gathers each step): all_starts is [U][U+W+2] u32 where rank p's
+ * bucket b (RW to server b for b < U, Flex to slot b-U for U <= b < U+W,
+ * local b = U+W) spans [all_starts[p][b], all_starts[p][b+1]).  Outputs
+ * 2*U entries each ([2p] RW part, [2p+1] Flex part), in elements: send
+ * offsets/counts into this rank's bucket-ordered buffer, receive
+ * offsets/counts into a buffer ordered by source rank; *recv_before = the
+ * number of received entries from ranks < g, *recv_total the sum. */
+ts_status ts_exchange_plan(uint32_t num_nodes, uint32_t gpus_per_node, uint32_t rank,
+                           const uint32_t* all_starts, uint64_t* send_off,
+                           uint64_t* send_cnt, uint64_t* recv_off, uint64_t* recv_cnt,
+                           uint64_t* recv_before, uint64_t* recv_total);
+
+/* ------------------------------------------------------------------------
  * Sharded sequence-embedding table: lookup (forward) and update (backward)
  * for one rank of a U = N*W GPU job.  Rank g stores, in one contiguous fp32
  * [local_rows x dim] shard: the dp_cut DP rows, the Flex rows of slot g % W,

@@ -50,6 +50,8 @@ EXPORTS = (
     "ts_router_iteration",
     "ts_router_iteration_device",
     "ts_router_destroy",
+    "ts_shard_layout",
+    "ts_exchange_plan",
     "ts_table_create",
     "ts_table_destroy",
     "ts_table_shard_rows",
@@ -127,6 +129,10 @@ def load() -> C.CDLL:
         "ts_router_iteration": (C.c_int, [vp, C.c_uint32, vp, vp, C.c_uint64, vp]),
         "ts_router_iteration_device": (C.c_int, [vp, vp, vp, C.c_uint64, vp]),
         "ts_router_destroy": (C.c_int, [vp]),
+        "ts_shard_layout": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, vp, C.c_uint32, C.c_uint32,
+                                      C.c_uint32, vp, u64p, u64p, u64p]),
+        "ts_exchange_plan": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, vp, vp, vp, vp, vp, u64p,
+                                       u64p]),
         "ts_table_create": (C.c_int, [C.POINTER(vp), C.POINTER(TableConfig), vp]),
         "ts_table_destroy": (C.c_int, [vp]),
         "ts_table_shard_rows": (C.c_int, [vp, u64p, u64p, u64p]),
@@ -179,6 +185,32 @@ def nccl_unique_id() -> bytes:
 
 def kernel_launches() -> int:
     return int(load().ts_kernel_launches())
+
+
+def shard_layout(n_rows, dp_cut, flex_cut, tier_dest, num_nodes, gpus_per_node, rank,
+                 with_ids=True):
+    """Host-only: (local_id[n] or None, (dp_rows, flex_rows, rw_rows)) of `rank`."""
+    dest = np.ascontiguousarray(tier_dest, dtype=np.uint8)
+    ids = np.zeros(n_rows, np.uint32) if with_ids else None
+    a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    _check(load().ts_shard_layout(n_rows, dp_cut, flex_cut, _ptr(dest) if dest.size else None,
+                                  num_nodes, gpus_per_node, rank,
+                                  _ptr(ids) if ids is not None and ids.size else None,
+                                  C.byref(a), C.byref(b), C.byref(c)))
+    return ids, (a.value, b.value, c.value)
+
+
+def exchange_plan(num_nodes, gpus_per_node, rank, all_starts):
+    """Host-only all-to-allv plan of `rank` from [U][U+W+2] bucket starts."""
+    u = num_nodes * gpus_per_node
+    st = np.ascontiguousarray(all_starts, dtype=np.uint32)
+    assert st.shape == (u, u + gpus_per_node + 2)
+    so, sc, ro, rc = (np.zeros(2 * u, np.uint64) for _ in range(4))
+    before, total = C.c_uint64(), C.c_uint64()
+    _check(load().ts_exchange_plan(num_nodes, gpus_per_node, rank, _ptr(st), _ptr(so), _ptr(sc),
+                                   _ptr(ro), _ptr(rc), C.byref(before), C.byref(total)))
+    return dict(send_off=so, send_cnt=sc, recv_off=ro, recv_cnt=rc, recv_before=before.value,
+                recv_total=total.value)
 
 
 class Router:

@@ -1,0 +1,34 @@
+// Host-only shard-layout and exchange-plan arithmetic (layout.cpp).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tiershard_b200.h"
+
+namespace tsd {
+
+struct LayoutError : std::runtime_error {
+  ts_status status;
+  LayoutError(ts_status st, const std::string& m) : std::runtime_error(m), status(st) {}
+};
+
+struct ShardRows {
+  uint64_t dp = 0, flex = 0, rw = 0;
+};
+
+// local_id may be nullptr (counts only).
+void shard_layout(uint64_t n, uint64_t dp_cut, uint64_t flex_cut, const uint8_t* dest, uint32_t N,
+                  uint32_t W, uint32_t g, uint32_t* local_id, ShardRows* rows);
+
+struct ExchangePlan {
+  std::vector<uint64_t> send_off, send_cnt, recv_off, recv_cnt;  // 2*U, [2p] RW, [2p+1] Flex
+  uint64_t recv_before = 0, recv_total = 0, n_remote = 0;
+};
+
+// all_starts: [U][U+W+2] bucket starts of every rank.
+void exchange_plan(uint32_t N, uint32_t W, uint32_t g, const uint32_t* all_starts, ExchangePlan* x);
+
+}  // namespace tsd

@@ -33,6 +33,7 @@
 #include "common.cuh"
 #include "embedding.cuh"
 #include "primitives.cuh"
+#include "layout.hpp"
 #include "route.cuh"
 
 namespace tsd {
@@ -251,28 +252,16 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
   } else {
     const uint64_t n = c.n_rows;
     h_dest.assign(tier_dest, tier_dest + n);
-    std::vector<uint64_t> flex_total(W, 0), rw_total(U, 0);
-    for (uint64_t i = c.dp_cut; i < c.flex_cut; ++i) {
-      if (tier_dest[i] >= W) fail(TS_ERR_VALIDATION, "table: Flex slot byte out of range");
-      ++flex_total[tier_dest[i]];
-    }
-    for (uint64_t i = c.flex_cut; i < n; ++i) {
-      if (tier_dest[i] >= U) fail(TS_ERR_VALIDATION, "table: RW owner byte out of range");
-      ++rw_total[tier_dest[i]];
-    }
     h_local.assign(n, 0);
-    std::vector<uint64_t> flex_next(W, 0), rw_next(U, 0);
-    for (uint64_t i = 0; i < c.dp_cut; ++i) h_local[i] = static_cast<uint32_t>(i);
-    for (uint64_t i = c.dp_cut; i < c.flex_cut; ++i) {
-      h_local[i] = static_cast<uint32_t>(c.dp_cut + flex_next[tier_dest[i]]++);
+    ShardRows sr;
+    try {
+      shard_layout(n, c.dp_cut, c.flex_cut, tier_dest, N, W, g, h_local.data(), &sr);
+    } catch (const LayoutError& e) {
+      fail(e.status, e.what());
     }
-    for (uint64_t i = c.flex_cut; i < n; ++i) {
-      const uint8_t o = tier_dest[i];
-      h_local[i] = static_cast<uint32_t>(c.dp_cut + flex_total[o % W] + rw_next[o]++);
-    }
-    dp_rows = c.dp_cut;
-    flex_rows = flex_total[slot];
-    rw_rows = rw_total[g];
+    dp_rows = sr.dp;
+    flex_rows = sr.flex;
+    rw_rows = sr.rw;
     local_rows = dp_rows + flex_rows + rw_rows;
     l2c.resize(local_rows);
     for (uint64_t i = 0; i < c.dp_cut; ++i) l2c[i] = static_cast<uint32_t>(i);
@@ -418,49 +407,20 @@ void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
                              cudaMemcpyDeviceToHost, stream));
     TSD_CUDA(cudaStreamSynchronize(stream));
   }
-  // h_counts holds every rank's bucket starts ([rank][nb + 1]); bucket b of
-  // rank p spans [start(p,b), start(p,b+1)), start(p, nb) == that rank's occ.
-  auto start_of = [&](uint32_t p, uint32_t b) -> uint64_t {
-    return h_counts[size_t{p} * (nb() + 1) + b];
-  };
-  auto count_of = [&](uint32_t p, uint32_t b) -> uint64_t { return start_of(p, b + 1) - start_of(p, b); };
-  const uint32_t local_b = U + W;
-  n_remote = start_of(g, local_b);
+  // Send layout: my remote buckets are contiguous in bucket order (RW by
+  // server, then Flex by slot); receive layout is ordered by source rank
+  // [p: RW from p | Flex from p] so server entries keep global occurrence
+  // order.  layout.cpp computes both (unit-tested on the CPU).
+  ExchangePlan xp;
+  exchange_plan(N, W, g, h_counts.data(), &xp);
+  send_off = xp.send_off;
+  send_cnt = xp.send_cnt;
+  recv_off = xp.recv_off;
+  recv_cnt = xp.recv_cnt;
+  recv_before = xp.recv_before;
+  recv_total = xp.recv_total;
+  n_remote = xp.n_remote;
   n_local_occ = occ - n_remote;
-
-  // send layout: per peer [RW part | Flex part] taken from my buckets; my
-  // remote buckets are contiguous in bucket order, which is exactly
-  // RW-by-server then Flex-by-slot.  NCCL gets per-peer offsets directly.
-  send_off.assign(2 * U, 0);
-  send_cnt.assign(2 * U, 0);
-  recv_off.assign(2 * U, 0);
-  recv_cnt.assign(2 * U, 0);
-  for (uint32_t p = 0; p < U; ++p) {
-    send_off[2 * p] = start_of(g, p);
-    send_cnt[2 * p] = p == g ? 0 : count_of(g, p);
-    if (p / W == node && p != g) {
-      send_off[2 * p + 1] = start_of(g, U + p % W);
-      send_cnt[2 * p + 1] = count_of(g, U + p % W);
-    }
-  }
-  // receive layout ordered by source rank: [p: RW from p | Flex from p]
-  uint64_t acc = 0;
-  recv_before = 0;
-  for (uint32_t p = 0; p < U; ++p) {
-    if (p == g) {
-      recv_before = acc;
-      continue;
-    }
-    recv_off[2 * p] = acc;
-    recv_cnt[2 * p] = count_of(p, g);
-    acc += recv_cnt[2 * p];
-    if (p / W == node) {
-      recv_off[2 * p + 1] = acc;
-      recv_cnt[2 * p + 1] = count_of(p, U + slot);
-      acc += recv_cnt[2 * p + 1];
-    }
-  }
-  recv_total = acc;
   recv_ids.ensure(recv_total);
   recv_rows.ensure(recv_total * cfg.dim);
 
