@@ -72,6 +72,22 @@ __device__ __forceinline__ void store_lane(float* p, const float (&r)[VEC]) {
   }
 }
 
+// Streaming (evict-first) store of one lane's slice: the unpooled output is
+// written once and not re-read before it has left L2 anyway, so it should
+// not evict the Zipf-hot weight rows.
+template <int VEC>
+__device__ __forceinline__ void store_lane_stream(float* p, const float (&r)[VEC]) {
+  if constexpr (VEC % 4 == 0) {
+#pragma unroll
+    for (int j = 0; j < VEC / 4; ++j) {
+      stg_stream(reinterpret_cast<float4*>(p + 4 * j),
+                 make_float4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]));
+    }
+  } else {
+    store_lane<VEC>(p, r);
+  }
+}
+
 // Canonical row -> local shard row of THIS rank, false if served remotely.
 __device__ __forceinline__ bool resolve_local(const RemapView& rv, uint32_t c, uint32_t* lid) {
   if (rv.identity || c < rv.dp_cut) {
@@ -110,7 +126,7 @@ gather_local_kernel(const uint32_t* __restrict__ rows, uint64_t occ,
 #pragma unroll
     for (int k = 0; k < UNROLL; ++k) {
       if (ok[k]) {
-        store_lane<VEC>(out + (base + k) * DIM + lane * VEC, r[k]);
+        store_lane_stream<VEC>(out + (base + k) * DIM + lane * VEC, r[k]);
 #pragma unroll
         for (int j = 0; j < VEC; ++j) sq = __fmaf_rn(r[k][j], r[k][j], sq);
       }
@@ -128,12 +144,20 @@ gather_local_kernel(const uint32_t* __restrict__ rows, uint64_t occ,
   }
 }
 
-__global__ void loss_finalize_kernel(const double* __restrict__ partials, unsigned count,
-                                     double* __restrict__ loss) {
-  // one thread, fixed order: deterministic for a fixed grid
+// Fixed-shape tree over the partials (thread t sums t, t+1024, ... in order,
+// then a fixed shared-memory tree): deterministic for a fixed grid.
+__global__ void __launch_bounds__(1024)
+loss_finalize_kernel(const double* __restrict__ partials, unsigned count, double* __restrict__ loss) {
+  __shared__ double s[1024];
   double acc = 0.0;
-  for (unsigned i = 0; i < count; ++i) acc += partials[i];
-  *loss = 0.5 * acc;
+  for (unsigned i = threadIdx.x; i < count; i += 1024) acc += partials[i];
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (unsigned half = 512; half > 0; half >>= 1) {
+    if (threadIdx.x < half) s[threadIdx.x] += s[threadIdx.x + half];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *loss = 0.5 * s[0];
 }
 
 // ---------------------------------------------------------------------------
@@ -217,6 +241,101 @@ __device__ __forceinline__ void sum_entries(const uint32_t* __restrict__ vals, u
   }
 }
 
+// ---------------------------------------------------------------------------
+// Short segments, several per warp.  A group of G lanes owns one segment; lane
+// l of the group holds the PER = DIM/G contiguous floats [l*PER, (l+1)*PER),
+// i.e. the K = 32/G "virtual lanes" l*K .. l*K+K-1 of the oracle's 32-lane
+// layout (V = DIM/32 floats each).  The Adagrad sum of squares is formed per
+// virtual lane and combined by the same xor butterfly (levels 16..1 over the
+// virtual index: cross-lane shuffles for m >= K, in-register for m < K), so
+// the result is bit-identical to restate.c.
+// ---------------------------------------------------------------------------
+
+template <int DIM>
+struct Grouping {
+  static constexpr int G = DIM <= 128 ? 8 : (DIM == 256 ? 16 : 32);  // lanes per segment
+  static constexpr int PER = DIM / G;                                 // floats per lane
+  static constexpr int K = 32 / G;                                    // virtual lanes per lane
+  static constexpr int V = DIM / 32;                                  // floats per virtual lane
+  static constexpr int E = PER <= 8 ? 4 : (PER <= 16 ? 2 : 1);        // entries in flight
+};
+
+template <int PER>
+__device__ __forceinline__ void load_vec(const float* p, float (&r)[PER]) {
+  static_assert(PER % 4 == 0, "group lanes hold whole float4s");
+#pragma unroll
+  for (int j = 0; j < PER / 4; ++j) {
+    const float4 t = *reinterpret_cast<const float4*>(p + 4 * j);
+    r[4 * j] = t.x;
+    r[4 * j + 1] = t.y;
+    r[4 * j + 2] = t.z;
+    r[4 * j + 3] = t.w;
+  }
+}
+
+template <int PER>
+__device__ __forceinline__ void store_vec(float* p, const float (&r)[PER]) {
+#pragma unroll
+  for (int j = 0; j < PER / 4; ++j) {
+    *reinterpret_cast<float4*>(p + 4 * j) = make_float4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+  }
+}
+
+template <int DIM>
+__device__ __forceinline__ void group_finish_row(uint32_t row, const float (&g)[Grouping<DIM>::PER],
+                                                 unsigned gl, unsigned gmask,
+                                                 float* __restrict__ weights,
+                                                 float* __restrict__ state, const OptParams& opt,
+                                                 const DenseRange& d0, const DenseRange& d1) {
+  using Gp = Grouping<DIM>;
+  constexpr int PER = Gp::PER, K = Gp::K, V = Gp::V;
+  const uint64_t col = static_cast<uint64_t>(gl) * PER;
+  if (row >= d0.lo && row < d0.hi) {
+    store_vec<PER>(d0.grad + static_cast<uint64_t>(row - d0.lo) * DIM + col, g);
+    return;
+  }
+  if (row >= d1.lo && row < d1.hi) {
+    store_vec<PER>(d1.grad + static_cast<uint64_t>(row - d1.lo) * DIM + col, g);
+    return;
+  }
+  float* wp = weights + static_cast<uint64_t>(row) * DIM + col;
+  float w[PER];
+  load_vec<PER>(wp, w);
+  if (opt.optimizer == TS_OPT_SGD) {
+#pragma unroll
+    for (int j = 0; j < PER; ++j) w[j] = __fmaf_rn(-opt.lr, g[j], w[j]);
+  } else {
+    float q[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc = __fmaf_rn(g[k * V + j], g[k * V + j], acc);
+      q[k] = acc;
+    }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      if (m >= K) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) q[k] = __fadd_rn(q[k], __shfl_xor_sync(gmask, q[k], m / K));
+      } else {
+        float nq[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) nq[k] = __fadd_rn(q[k], q[k ^ m]);
+#pragma unroll
+        for (int k = 0; k < K; ++k) q[k] = nq[k];
+      }
+    }
+    const float G = __fadd_rn(state[row], __fdiv_rn(q[0], static_cast<float>(DIM)));
+    __syncwarp(gmask);
+    if (gl == 0) state[row] = G;
+    const float denom = __fadd_rn(__fsqrt_rn(G), opt.eps);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) w[j] = __fmaf_rn(-opt.lr, __fdiv_rn(g[j], denom), w[j]);
+  }
+  store_vec<PER>(wp, w);
+}
+
 template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 seg_short_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
@@ -224,19 +343,42 @@ seg_short_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__
                  GradSource gs, float* __restrict__ weights, float* __restrict__ state,
                  OptParams opt, DenseRange d0, DenseRange d1, uint32_t* __restrict__ long_list,
                  uint32_t* __restrict__ long_count) {
+  using Gp = Grouping<DIM>;
+  constexpr int G = Gp::G, PER = Gp::PER, E = Gp::E;
   const unsigned lane = threadIdx.x & 31u;
+  const unsigned group = lane / G, gl = lane % G;
+  const unsigned gmask = G == 32 ? 0xFFFFFFFFu : (((1u << G) - 1u) << (group * G));
   const uint32_t nseg = *d_nseg;
-  const uint32_t gwarp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
-  for (uint32_t j = gwarp; j < nseg; j += nwarps) {
+  const uint32_t gid = ((blockIdx.x * kThreads + threadIdx.x) >> 5) * (32 / G) + group;
+  const uint32_t ngroups = ((gridDim.x * kThreads) >> 5) * (32 / G);
+  const uint64_t col = static_cast<uint64_t>(gl) * PER;
+  for (uint32_t j = gid; j < nseg; j += ngroups) {
     const uint32_t s = __ldg(starts + j), e = __ldg(starts + j + 1);
     if (e - s > kPiece) {
-      if (lane == 0) long_list[atomicAdd(long_count, 1u)] = j;
+      if (gl == 0) long_list[atomicAdd(long_count, 1u)] = j;
       continue;
     }
-    float acc[DIM / 32];
-    sum_entries<DIM>(vals, s, e, gs, acc);
-    finish_row<DIM>(__ldg(keys + s), acc, weights, state, opt, d0, d1);
+    const uint32_t row = __ldg(keys + s);
+    float acc[PER];
+    load_vec<PER>(grad_row<1>(gs, __ldg(vals + s), DIM) + col, acc);
+    uint32_t k = s + 1;
+    for (; k + E <= e; k += E) {
+      float r[E][PER];
+#pragma unroll
+      for (int b = 0; b < E; ++b) load_vec<PER>(grad_row<1>(gs, __ldg(vals + k + b), DIM) + col, r[b]);
+#pragma unroll
+      for (int b = 0; b < E; ++b) {
+#pragma unroll
+        for (int q = 0; q < PER; ++q) acc[q] = __fadd_rn(acc[q], r[b][q]);
+      }
+    }
+    for (; k < e; ++k) {
+      float r[PER];
+      load_vec<PER>(grad_row<1>(gs, __ldg(vals + k), DIM) + col, r);
+#pragma unroll
+      for (int q = 0; q < PER; ++q) acc[q] = __fadd_rn(acc[q], r[q]);
+    }
+    group_finish_row<DIM>(row, acc, gl, gmask, weights, state, opt, d0, d1);
   }
 }
 
@@ -396,7 +538,7 @@ void launch_gather_local(const uint32_t* rows, uint64_t occ, const float* weight
 }
 
 void launch_loss_finalize(const double* partials, unsigned count, double* loss, cudaStream_t stream) {
-  loss_finalize_kernel<<<1, 1, 0, stream>>>(partials, count, loss);
+  loss_finalize_kernel<<<1, 1024, 0, stream>>>(partials, count, loss);
   TSD_LAUNCH_CHECK();
 }
 

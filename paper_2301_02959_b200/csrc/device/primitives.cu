@@ -66,33 +66,101 @@ scan_apply_kernel(const uint32_t* in, uint32_t* out, uint64_t n, const uint32_t*
 }
 
 // ---------------------------------------------------------------------------
-// radix sort
+// onesweep radix sort: one global histogram for every pass, then one kernel
+// per pass that ranks its tile, finds the tile's per-digit prefix with a
+// decoupled look-back over earlier tiles, and scatters.  Each pass reads the
+// pairs once and writes them once (the classic hist + scan + scatter pass
+// reads the keys twice and scans 256 x tiles counts).
 // ---------------------------------------------------------------------------
 
-__global__ void __launch_bounds__(kRadixThreads)
-radix_hist_kernel(const uint32_t* __restrict__ keys, uint64_t n, int shift, uint32_t mask,
-                  uint32_t* __restrict__ hist, uint32_t tiles) {
-  __shared__ uint32_t s_h[kRadixBins];
-  s_h[threadIdx.x] = 0;
-  __syncthreads();
-  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRadixTile;
-#pragma unroll 4
-  for (int k = 0; k < kRadixItems; ++k) {
-    const uint64_t i = base + static_cast<uint64_t>(k) * kRadixThreads + threadIdx.x;
-    const bool valid = i < n;
-    const uint32_t d = valid ? (keys[i] >> shift) & mask : 0xFFFFFFFFu;
-    // Zipf-skewed keys put many equal digits in one warp: aggregate first.
-    const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
-    if (valid && (peers & lanemask_lt()) == 0) atomicAdd(&s_h[d], __popc(peers));
+// Lanes of the warp whose digit equals mine (warp multi-split by one ballot
+// per digit bit — cheaper than __match_any_sync on sm_100).  Lanes with
+// valid == false match nobody and get 0.
+__device__ __forceinline__ unsigned digit_peers(uint32_t d, bool valid, int bits) {
+  unsigned peers = __ballot_sync(0xFFFFFFFFu, valid);
+  for (int b = 0; b < bits; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const unsigned ones = __ballot_sync(0xFFFFFFFFu, bit);
+    peers &= bit ? ones : ~ones;
   }
-  __syncthreads();
-  hist[static_cast<uint64_t>(threadIdx.x) * tiles + blockIdx.x] = s_h[threadIdx.x];
+  return valid ? peers : 0u;
 }
 
+// True when every lane of the warp is valid and holds the same digit (the
+// common case in the high-order passes of Zipf-skewed row ids).
+__device__ __forceinline__ bool warp_uniform(uint32_t d, bool valid) {
+  const uint32_t d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
+  return __all_sync(0xFFFFFFFFu, valid && d == d0);
+}
+
+constexpr uint64_t kFlagAgg = 1ull << 62;   // tile-local count published
+constexpr uint64_t kFlagInc = 2ull << 62;   // inclusive prefix published
+constexpr uint64_t kCountMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ int pass_bits(int key_bits, int pass) {
+  const int left = key_bits - 8 * pass;
+  return left < 8 ? left : 8;
+}
+
+// Digit histograms of every pass from ONE read of the keys.  Warps whose
+// digits all agree add 32 at once; otherwise plain shared atomics (few
+// conflicts when digits are spread).
 __global__ void __launch_bounds__(kRadixThreads)
-radix_scatter_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
-                     uint64_t n, int shift, uint32_t mask, const uint32_t* __restrict__ hist,
-                     const uint32_t* __restrict__ hist_scan, uint32_t tiles,
+onesweep_hist_kernel(const uint32_t* __restrict__ keys, uint64_t n, int key_bits, int passes,
+                     uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t s_h[kMaxRadixPasses][kRadixBins];
+  for (int p = 0; p < passes; ++p) s_h[p][threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRadixTile;
+  const unsigned lane = threadIdx.x & 31u;
+  uint32_t key[kRadixItems];
+#pragma unroll
+  for (int k = 0; k < kRadixItems; ++k) {
+    const uint64_t i = base + static_cast<uint64_t>(k) * kRadixThreads + threadIdx.x;
+    key[k] = i < n ? __ldg(keys + i) : 0u;
+  }
+  for (int p = 0; p < passes; ++p) {
+    const uint32_t mask = (1u << pass_bits(key_bits, p)) - 1u;
+#pragma unroll
+    for (int k = 0; k < kRadixItems; ++k) {
+      const bool valid = base + static_cast<uint64_t>(k) * kRadixThreads + threadIdx.x < n;
+      const uint32_t d = (key[k] >> (8 * p)) & mask;
+      if (warp_uniform(d, valid)) {
+        if (lane == 0) atomicAdd(&s_h[p][d], 32u);
+      } else if (valid) {
+        atomicAdd(&s_h[p][d], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  for (int p = 0; p < passes; ++p) {
+    if (s_h[p][threadIdx.x]) atomicAdd(ghist + p * kRadixBins + threadIdx.x, s_h[p][threadIdx.x]);
+  }
+}
+
+// Exclusive scan of each pass's 256 digit totals (one block per pass).
+__global__ void __launch_bounds__(kRadixThreads)
+onesweep_offsets_kernel(const uint32_t* __restrict__ ghist, uint32_t* __restrict__ goff) {
+  __shared__ uint32_t s_warp[kRadixThreads / 32 + 1];
+  const int p = blockIdx.x;
+  uint32_t total;
+  goff[p * kRadixBins + threadIdx.x] =
+      block_exclusive_scan<kRadixThreads>(ghist[p * kRadixBins + threadIdx.x], s_warp, &total);
+}
+
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(kRadixThreads, 3)
+onesweep_pass_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+                     uint64_t n, int shift, int bits, const uint32_t* __restrict__ goff,
+                     uint64_t* __restrict__ status, uint32_t* __restrict__ tile_counter,
                      uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
   __shared__ uint32_t s_keys[kRadixTile];
   __shared__ uint32_t s_vals[kRadixTile];
@@ -100,19 +168,18 @@ radix_scatter_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __res
   __shared__ uint32_t s_tile_excl[kRadixBins];
   __shared__ uint32_t s_gbase[kRadixBins];
   __shared__ uint32_t s_warp[kRadixThreads / 32 + 1];
+  __shared__ uint32_t s_tile;
 
+  const uint32_t mask = (1u << bits) - 1u;
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  const uint64_t tile_base = static_cast<uint64_t>(blockIdx.x) * kRadixTile;
-
+  // Dynamic tile ids in launch order: every predecessor of a tile was
+  // scheduled before it, so the look-back below always makes progress.
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
 #pragma unroll
   for (int w = 0; w < kRadixWarps; ++w) s_run[w][threadIdx.x] = 0;
-  {
-    const uint64_t hi = static_cast<uint64_t>(threadIdx.x) * tiles + blockIdx.x;
-    uint32_t total;
-    s_tile_excl[threadIdx.x] = block_exclusive_scan<kRadixThreads>(hist[hi], s_warp, &total);
-    s_gbase[threadIdx.x] = hist_scan[hi];
-  }
   __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t tile_base = static_cast<uint64_t>(tile) * kRadixTile;
 
   uint32_t k[kRadixItems], v[kRadixItems], rank[kRadixItems];
   const uint64_t sub_base = tile_base + static_cast<uint64_t>(warp) * kRadixSubTile;
@@ -120,33 +187,83 @@ radix_scatter_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __res
   for (int r = 0; r < kRadixItems; ++r) {
     const uint64_t i = sub_base + static_cast<uint64_t>(r) * 32 + lane;
     const bool valid = i < n;
-    k[r] = valid ? keys_in[i] : 0u;
-    v[r] = valid ? (vals_in ? vals_in[i] : static_cast<uint32_t>(i)) : 0u;
-    const uint32_t d = valid ? (k[r] >> shift) & mask : 0xFFFFFFFFu;
-    const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
-    rank[r] = valid ? s_run[warp][d] + __popc(peers & lanemask_lt()) : 0u;
-    __syncwarp();
-    if (valid && (peers & lanemask_lt()) == 0) s_run[warp][d] += __popc(peers);
+    k[r] = valid ? __ldg(keys_in + i) : 0u;
+    v[r] = valid ? (vals_in ? __ldg(vals_in + i) : static_cast<uint32_t>(i)) : 0u;
+  }
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int r = 0; r < kRadixItems; ++r) {
+    const bool valid = sub_base + static_cast<uint64_t>(r) * 32 + lane < n;
+    const uint32_t d = (k[r] >> shift) & mask;
+    if (warp_uniform(d, valid)) {
+      rank[r] = s_run[warp][d] + lane;
+      __syncwarp();
+      if (lane == 0) s_run[warp][d] += 32u;
+    } else {
+      const unsigned peers = digit_peers(d, valid, bits);
+      rank[r] = valid ? s_run[warp][d] + __popc(peers & lt) : 0u;
+      __syncwarp();
+      if (valid && (peers & lt) == 0) s_run[warp][d] += __popc(peers);
+    }
     __syncwarp();
   }
   __syncthreads();
-  {
-    // order the warps' sub-tiles: per digit, prefix over warps
-    uint32_t acc = s_tile_excl[threadIdx.x];
+
+  // Per digit (thread = digit): tile count, warp prefix, look-back.
+  const uint32_t d = threadIdx.x;
+  uint32_t count = 0;
 #pragma unroll
-    for (int w = 0; w < kRadixWarps; ++w) {
-      const uint32_t t = s_run[w][threadIdx.x];
-      s_run[w][threadIdx.x] = acc;
-      acc += t;
-    }
+  for (int w = 0; w < kRadixWarps; ++w) {
+    const uint32_t t = s_run[w][d];
+    s_run[w][d] = count;
+    count += t;
   }
+  uint64_t* my = status + static_cast<uint64_t>(tile) * kRadixBins + d;
+  uint64_t excl = 0;
+  if (tile == 0) {
+    st_relaxed_u64(my, kFlagInc | count);
+  } else {
+    st_relaxed_u64(my, kFlagAgg | count);
+    // Windowed look-back: kWindow predecessor words in flight at once, then
+    // consumed nearest-first until an inclusive prefix is found; a
+    // not-yet-published word restarts the window at that tile.
+    constexpr int kWindow = 8;
+    int64_t p = static_cast<int64_t>(tile) - 1;
+    bool done = false;
+    while (!done) {
+      uint64_t s[kWindow];
+#pragma unroll
+      for (int w = 0; w < kWindow; ++w) {
+        s[w] = p - w >= 0 ? ld_relaxed_u64(status + static_cast<uint64_t>(p - w) * kRadixBins + d)
+                          : kFlagInc;
+      }
+      int used = 0;
+#pragma unroll
+      for (int w = 0; w < kWindow; ++w) {
+        if (done || used != w) break;
+        const uint64_t flag = s[w] & ~kCountMask;
+        if (flag == 0) break;  // not ready: re-poll from here
+        excl += s[w] & kCountMask;
+        done = flag == kFlagInc;
+        ++used;
+      }
+      p -= used;
+    }
+    st_relaxed_u64(my, kFlagInc | (excl + count));
+  }
+  uint32_t total;
+  const uint32_t tile_excl = block_exclusive_scan<kRadixThreads>(count, s_warp, &total);
+  s_tile_excl[d] = tile_excl;
+  s_gbase[d] = goff[d] + static_cast<uint32_t>(excl);
+#pragma unroll
+  for (int w = 0; w < kRadixWarps; ++w) s_run[w][d] += tile_excl;
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kRadixItems; ++r) {
     const uint64_t i = sub_base + static_cast<uint64_t>(r) * 32 + lane;
     if (i < n) {
-      const uint32_t d = (k[r] >> shift) & mask;
-      const uint32_t pos = s_run[warp][d] + rank[r];
+      const uint32_t dd = (k[r] >> shift) & mask;
+      const uint32_t pos = s_run[warp][dd] + rank[r];
       s_keys[pos] = k[r];
       s_vals[pos] = v[r];
     }
@@ -156,8 +273,8 @@ radix_scatter_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __res
   const uint32_t tile_n = left < kRadixTile ? static_cast<uint32_t>(left) : kRadixTile;
   for (uint32_t j = threadIdx.x; j < tile_n; j += kRadixThreads) {
     const uint32_t kk = s_keys[j];
-    const uint32_t d = (kk >> shift) & mask;
-    const uint32_t dst = s_gbase[d] + (j - s_tile_excl[d]);
+    const uint32_t dd = (kk >> shift) & mask;
+    const uint32_t dst = s_gbase[dd] + (j - s_tile_excl[dd]);
     keys_out[dst] = kk;
     vals_out[dst] = s_vals[j];
   }
@@ -233,26 +350,30 @@ void radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t
                       cudaStream_t stream) {
   // Even passes write (keys_a, vals_a), odd passes (keys_b, vals_b); the
   // caller's input is only read.
-  const uint32_t* cur_k = keys_in;
-  const uint32_t* cur_v = vals_in;
   *keys_out = buf.keys_a;
   *vals_out = buf.vals_a;
   if (n == 0) return;
-  const uint32_t tiles = static_cast<uint32_t>(radix_tiles(n));
   if (key_bits < 1) key_bits = 1;
-  int pass = 0;
-  for (int shift = 0; shift < key_bits; shift += 8, ++pass) {
+  if (key_bits > 32) key_bits = 32;
+  const int passes = (key_bits + 7) / 8;
+  const uint32_t tiles = static_cast<uint32_t>(radix_tiles(n));
+  TSD_CUDA(cudaMemsetAsync(buf.ghist, 0, sizeof(uint32_t) * kMaxRadixPasses * kRadixBins, stream));
+  TSD_CUDA(cudaMemsetAsync(buf.counters, 0, sizeof(uint32_t) * kMaxRadixPasses, stream));
+  TSD_CUDA(cudaMemsetAsync(buf.status, 0, sizeof(uint64_t) * passes * tiles * kRadixBins, stream));
+  onesweep_hist_kernel<<<tiles, kRadixThreads, 0, stream>>>(keys_in, n, key_bits, passes, buf.ghist);
+  TSD_LAUNCH_CHECK();
+  onesweep_offsets_kernel<<<passes, kRadixThreads, 0, stream>>>(buf.ghist, buf.goff);
+  TSD_LAUNCH_CHECK();
+  const uint32_t* cur_k = keys_in;
+  const uint32_t* cur_v = vals_in;
+  for (int pass = 0; pass < passes; ++pass) {
+    const int shift = 8 * pass;
     const int bits = key_bits - shift < 8 ? key_bits - shift : 8;
-    const uint32_t mask = (1u << bits) - 1u;
     uint32_t* out_k = (pass & 1) ? buf.keys_b : buf.keys_a;
     uint32_t* out_v = (pass & 1) ? buf.vals_b : buf.vals_a;
-    radix_hist_kernel<<<tiles, kRadixThreads, 0, stream>>>(cur_k, n, shift, mask, buf.hist, tiles);
-    TSD_LAUNCH_CHECK();
-    device_exclusive_scan(buf.hist, buf.hist_scan, static_cast<uint64_t>(kRadixBins) * tiles,
-                          buf.scan_scratch, nullptr, stream);
-    radix_scatter_kernel<<<tiles, kRadixThreads, 0, stream>>>(cur_k, cur_v, n, shift, mask,
-                                                              buf.hist, buf.hist_scan, tiles,
-                                                              out_k, out_v);
+    onesweep_pass_kernel<<<tiles, kRadixThreads, 0, stream>>>(
+        cur_k, cur_v, n, shift, bits, buf.goff + pass * kRadixBins,
+        buf.status + static_cast<uint64_t>(pass) * tiles * kRadixBins, buf.counters + pass, out_k, out_v);
     TSD_LAUNCH_CHECK();
     cur_k = out_k;
     cur_v = out_v;

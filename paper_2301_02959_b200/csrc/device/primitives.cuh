@@ -2,16 +2,19 @@
 // compaction): warp/block scans, a device exclusive scan, and a stable LSD
 // radix sort of (u32 key, u32 value) pairs.
 //
-// Radix sort design (sm_100a, HBM-bound): per 8-bit pass
-//   1. radix_hist     — per-tile digit histogram, written digit-major
-//                       [256][tiles] so one exclusive scan yields every
-//                       (digit, tile) output base;
-//   2. scan           — device exclusive scan of the 256*tiles counts;
-//   3. radix_scatter  — stable in-tile ranking (each warp ranks its own
-//                       contiguous 512-item sub-tile with __match_any_sync,
-//                       warps are ordered by a per-digit prefix), the tile is
-//                       staged digit-sorted in shared memory and then written
-//                       out in coalesced runs.
+// Radix sort design (sm_100a, HBM-bound), "onesweep":
+//   1. onesweep_hist    — ONE read of the keys builds the 256-bin histograms of
+//                         every 8-bit pass (warp match_any aggregation);
+//   2. onesweep_offsets — exclusive scan per pass -> global digit offsets;
+//   3. onesweep_pass    — per pass, per 4096-item tile: stable in-tile ranking
+//                         (each warp ranks its contiguous 512-item sub-tile
+//                         with __match_any_sync; warps ordered by a per-digit
+//                         prefix), decoupled look-back over earlier tiles for
+//                         the tile's per-digit global offset (tile ids taken
+//                         from an atomic counter in launch order, so the
+//                         look-back always progresses), smem staging, then
+//                         coalesced run write-out.  One read + one write of the
+//                         pairs per pass.
 // Stability: ranks follow input order inside a warp sub-tile, sub-tiles follow
 // warp order, tiles follow tile order — so equal keys keep input order, which
 // is what makes the segment sums deterministic (oracle/restate.h).
@@ -44,14 +47,18 @@ inline uint64_t radix_tiles(uint64_t n) { return (n + kRadixTile - 1) / kRadixTi
 void device_exclusive_scan(const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* scratch,
                            uint32_t* d_total, cudaStream_t stream);
 
+constexpr int kMaxRadixPasses = 4;
+
 struct RadixBuffers {
-  uint32_t* keys_a;        // n
-  uint32_t* vals_a;        // n
-  uint32_t* keys_b;        // n
-  uint32_t* vals_b;        // n
-  uint32_t* hist;          // 256 * radix_tiles(n)
-  uint32_t* hist_scan;     // 256 * radix_tiles(n)
-  uint32_t* scan_scratch;  // scan_scratch_elems(256 * radix_tiles(n))
+  uint32_t* keys_a;    // n
+  uint32_t* vals_a;    // n
+  uint32_t* keys_b;    // n
+  uint32_t* vals_b;    // n
+  uint32_t* ghist;     // kMaxRadixPasses * 256 digit totals
+  uint32_t* goff;      // kMaxRadixPasses * 256 exclusive digit offsets (goff[0..] of pass 0
+                       // are the bucket starts when a single pass sorts bucket ids)
+  uint64_t* status;    // kMaxRadixPasses * radix_tiles(n) * 256 look-back words
+  uint32_t* counters;  // kMaxRadixPasses dynamic tile counters
 };
 
 // Stable sort of n (key, value) pairs by the low `key_bits` bits of the keys

@@ -116,7 +116,8 @@ struct ts_table {
   tsd::DevBuf<unsigned long long> tier_counts;  // RW, Flex, DP of this requester
   tsd::DevBuf<uint32_t> rows_dev;                // host-step staging
   // dedup / sort
-  tsd::DevBuf<uint32_t> keys_a, vals_a, keys_b, vals_b, hist, hist_scan, scan_scratch;
+  tsd::DevBuf<uint32_t> keys_a, vals_a, keys_b, vals_b, ghist, goff, sort_counters;
+  tsd::DevBuf<uint64_t> sort_status;
   tsd::DevBuf<uint32_t> starts, seg_scratch, nseg;
   tsd::DevBuf<uint32_t> long_list, long_count, piece_off, entry_keys, entry_vals;
   tsd::DevBuf<float> partials;
@@ -186,9 +187,10 @@ struct ts_table {
     keys_b.ensure(m);
     vals_b.ensure(m);
     const uint64_t tiles = tsd::radix_tiles(m);
-    hist.ensure(tiles * tsd::kRadixBins);
-    hist_scan.ensure(tiles * tsd::kRadixBins);
-    scan_scratch.ensure(tsd::scan_scratch_elems(tiles * tsd::kRadixBins) + 1);
+    ghist.ensure(tsd::kMaxRadixPasses * tsd::kRadixBins);
+    goff.ensure(tsd::kMaxRadixPasses * tsd::kRadixBins);
+    sort_counters.ensure(tsd::kMaxRadixPasses);
+    sort_status.ensure(tsd::kMaxRadixPasses * tiles * tsd::kRadixBins);
     starts.ensure(m + 1);
     seg_scratch.ensure(tsd::segment_scratch_elems(m) + 8);
     const uint64_t max_long = m / (tsd::kPiece + 1) + 1;
@@ -386,8 +388,8 @@ void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   bv.rank = g;
   bv.slot = slot;
   launch_bucket_keys(d_rows, occ, bv, bucket.ptr, tier_counts.ptr, stream);
-  RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, hist.ptr, hist_scan.ptr,
-                  scan_scratch.ptr};
+  RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, ghist.ptr, goff.ptr,
+                  sort_status.ptr, sort_counters.ptr};
   uint32_t* sorted_b = nullptr;
   uint32_t* sorted_i = nullptr;
   radix_sort_pairs(bucket.ptr, nullptr, occ, bits_for(nb() - 1), rb, &sorted_b, &sorted_i, stream);
@@ -399,7 +401,8 @@ void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   {
     const int passes = (bits_for(nb() - 1) + 7) / 8;
     if (passes != 1) fail(TS_ERR_CONFIG, "table: U + W + 1 must be <= 256 buckets");
-    launch_bucket_starts(hist_scan.ptr, radix_tiles(occ), nb(), static_cast<uint32_t>(occ),
+    // single counting pass: its global digit offsets ARE the bucket starts
+    launch_bucket_starts(goff.ptr, 1, nb(), static_cast<uint32_t>(occ),
                          bucket_start.ptr, stream);
     TSD_NCCL(ncclAllGather(bucket_start.ptr, all_counts.ptr, nb() + 1, ncclUint32, world, stream));
     h_counts.resize(static_cast<size_t>(U) * (nb() + 1));
@@ -506,8 +509,8 @@ void ts_table::backward(const float* d_grad) {
   last_entries = m;
 
   int t = phase_begin(kPhaseSort);
-  RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, hist.ptr, hist_scan.ptr,
-                  scan_scratch.ptr};
+  RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, ghist.ptr, goff.ptr,
+                  sort_status.ptr, sort_counters.ptr};
   uint32_t* sk = nullptr;
   uint32_t* sv = nullptr;
   radix_sort_pairs(keys_in, vals_in, m, bits_for(local_rows ? local_rows - 1 : 0), rb, &sk, &sv, stream);
@@ -565,7 +568,8 @@ void ts_table::destroy() {
   d_loss.release();
   tier_counts.release();
   rows_dev.release();
-  for (auto* b : {&keys_a, &vals_a, &keys_b, &vals_b, &hist, &hist_scan, &scan_scratch, &starts,
+  sort_status.release();
+  for (auto* b : {&keys_a, &vals_a, &keys_b, &vals_b, &ghist, &goff, &sort_counters, &starts,
                   &seg_scratch, &nseg, &long_list, &long_count, &piece_off, &entry_keys,
                   &entry_vals, &bucket, &order, &send_ids, &recv_ids, &bucket_start, &all_counts}) {
     b->release();
