@@ -510,6 +510,8 @@ def run_reference(args, dist: Dist):
 
 def main():
     args = parse_args()
+    # stdout carries exactly one JSON line: keep NCCL's banner off it
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     dist = Dist()
     try:
         if args.impl == "reference":

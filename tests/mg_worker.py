@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--nodes", type=int, required=True)
     ap.add_argument("--gpus-per-node", type=int, required=True)
     ap.add_argument("--optimizer", type=int, default=1)
+    ap.add_argument("--lr", type=float, default=1e-3)
     ap.add_argument("--out", required=True)
     args = ap.parse_args()
     import torch
@@ -52,7 +53,7 @@ def main():
     td.broadcast_object_list(box, src=0)
     table = ts.Table(n_rows=pb["n"], dim=pb["dim"], dp_cut=pb["dp_cut"], flex_cut=pb["flex_cut"],
                      tier_dest=pb["dest"], num_nodes=args.nodes, gpus_per_node=args.gpus_per_node,
-                     rank=rank, device=local, weight_seed=77, optimizer=args.optimizer, lr=0.05,
+                     rank=rank, device=local, weight_seed=77, optimizer=args.optimizer, lr=args.lr,
                      max_occurrences=int(pb["rows"][rank].size), nccl_unique_id=box[0])
     rows = pb["rows"][rank]
     d_rows = torch.from_numpy(rows.view(np.int32)).cuda()
