@@ -172,7 +172,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -220,6 +220,27 @@ PHASE_BYTES_DOC = {
                       "weight read+write, Adagrad state read+write",
     "dedup_sort": "passes x entries x 20: key read (histogram) + pair read + pair write",
 }
+
+
+PHASE_KERNELS = {
+    "gather": ["gather_local_kernel"],
+    "segment_update": ["seg_short_kernel", "long_prefix_kernel", "piece_kernel", "long_combine_kernel"],
+    "dedup_sort": ["onesweep_hist_kernel", "onesweep_offsets_kernel", "onesweep_pass_kernel"],
+}
+
+
+def ncu_traffic(phase, u):
+    """DRAM bytes (read + write) per launch of the phase's kernels, from the
+    committed ncu --set full capture summarised in profiles/ncu_traffic.json
+    (tools_traffic.py).  None when that capture does not cover the phase."""
+    try:
+        doc = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
+    except Exception:
+        return None, None
+    entry = doc.get("n1" if u == 1 else f"n{u}", {}).get(phase)
+    if not entry:
+        return None, None
+    return entry["dram_bytes_per_step"], doc.get("source")
 
 
 def measured_peaks():
@@ -271,14 +292,16 @@ def run_ours(args, dist: Dist):
         b = d_rows[k % len(d_rows)]
         table.train_step(b.data_ptr(), b.numel(), d_out.data_ptr())
 
+    # clocks are sampled from the warm-up through the e2e pass (the timed
+    # region is inside that window; only samples under load are reported)
+    clocks = ClockSampler(device)
+    clocks.start()
     for k in range(args.warmup):
         step(k)
     table.synchronize()
     dist.barrier()
 
     # ---- timed region: device-side, CUDA events on the table stream --------
-    clocks = ClockSampler(device)
-    clocks.start()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     launches0 = ts.kernel_launches()
@@ -311,7 +334,6 @@ def run_ours(args, dist: Dist):
         step(k)
     phases = table.phase_times()
     table.enable_timing(False)
-    clk = clocks.stop()
 
     # ---- end to end through the host-buffer public entry point -------------
     e2e = None
@@ -327,13 +349,22 @@ def run_ours(args, dist: Dist):
         h2d = float(np.mean([pinned[k % len(pinned)].nbytes for k in range(args.steps)]))
         e2e = {"value": samples / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 8}
+    clk = clocks.stop()
 
     # ---- roofline of the dominant kernel -----------------------------------
     row_bytes = D * 4
     occ_mean = float(np.mean([b.size for b in batches]))
     distinct = float(counters[6, g])
     entries = float(counters[5, g])
-    n_local_occ = occ_mean if u == 1 else float(counters[4, g] + counters[0, g] + counters[2, g])
+    if u == 1:
+        n_local_occ = occ_mean
+    else:  # DP rows, RW rows this rank owns, Flex rows of its slot
+        dp_c, fx_c = plan["dp_cut"], plan["flex_cut"]
+        loc = []
+        for b in batches:
+            d_b = dest[b]
+            loc.append(int(((b < dp_c) | ((b < fx_c) & (d_b == g % w)) | ((b >= fx_c) & (d_b == g))).sum()))
+        n_local_occ = float(np.mean(loc))
     key_bits = int(np.ceil(np.log2(max(2, exp["n_rows"] if u == 1 else exp["n_rows"] // u))))
     passes = (key_bits + 7) // 8
     algo = {
@@ -346,9 +377,12 @@ def run_ours(args, dist: Dist):
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     achieved = algo[dominant] / (per_launch_ms[dominant] / 1e3) / 1e9
-    roofline = {"bound": "hbm", "kernel": dominant, "achieved": round(achieved, 1),
+    traffic, traffic_src = ncu_traffic(dominant, u)
+    roofline = {"bound": "hbm", "kernel": dominant, "kernels": PHASE_KERNELS.get(dominant),
+                "achieved": round(achieved, 1),
                 "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
-                "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
+                "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
                 "algorithmic_bytes_per_launch": algo[dominant], "avg_launch_ms": per_launch_ms[dominant],
                 "bytes_model": PHASE_BYTES_DOC[dominant],
                 "all_phases_ms_per_step": {k: round(v[0] / max(1, v[1]), 4) for k, v in phases.items() if v[1]}}

@@ -339,7 +339,8 @@ __device__ __forceinline__ void group_finish_row(uint32_t row, const float (&g)[
 template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 seg_short_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
-                 const uint32_t* __restrict__ starts, const uint32_t* __restrict__ d_nseg,
+                 const uint32_t* __restrict__ starts, const uint32_t* __restrict__ d_lo,
+                 const uint32_t* __restrict__ d_hi,
                  GradSource gs, float* __restrict__ weights, float* __restrict__ state,
                  OptParams opt, DenseRange d0, DenseRange d1, uint32_t* __restrict__ long_list,
                  uint32_t* __restrict__ long_count) {
@@ -348,11 +349,11 @@ seg_short_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__
   const unsigned lane = threadIdx.x & 31u;
   const unsigned group = lane / G, gl = lane % G;
   const unsigned gmask = G == 32 ? 0xFFFFFFFFu : (((1u << G) - 1u) << (group * G));
-  const uint32_t nseg = *d_nseg;
+  const uint32_t seg_lo = *d_lo, seg_hi = *d_hi;
   const uint32_t gid = ((blockIdx.x * kThreads + threadIdx.x) >> 5) * (32 / G) + group;
   const uint32_t ngroups = ((gridDim.x * kThreads) >> 5) * (32 / G);
   const uint64_t col = static_cast<uint64_t>(gl) * PER;
-  for (uint32_t j = gid; j < nseg; j += ngroups) {
+  for (uint32_t j = seg_lo + gid; j < seg_hi; j += ngroups) {
     const uint32_t s = __ldg(starts + j), e = __ldg(starts + j + 1);
     if (e - s > kPiece) {
       if (gl == 0) long_list[atomicAdd(long_count, 1u)] = j;
@@ -542,9 +543,30 @@ void launch_loss_finalize(const double* partials, unsigned count, double* loss, 
   TSD_LAUNCH_CHECK();
 }
 
+// Number of segments whose key is < split_key (sorted keys, so a lower bound
+// over the segment heads); out[0] = 0, out[1] = split.
+__global__ void segment_split_kernel(const uint32_t* __restrict__ keys,
+                                     const uint32_t* __restrict__ starts,
+                                     const uint32_t* __restrict__ d_nseg, uint32_t split_key,
+                                     uint32_t* __restrict__ out) {
+  uint32_t lo = 0, hi = *d_nseg;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (keys[starts[mid]] < split_key) lo = mid + 1; else hi = mid;
+  }
+  out[0] = 0;
+  out[1] = lo;
+}
+
+void launch_segment_split(const uint32_t* keys, const uint32_t* starts, const uint32_t* d_nseg,
+                          uint32_t split_key, uint32_t* out, cudaStream_t stream) {
+  segment_split_kernel<<<1, 1, 0, stream>>>(keys, starts, d_nseg, split_key, out);
+  TSD_LAUNCH_CHECK();
+}
+
 void launch_segment_update(const uint32_t* keys, const uint32_t* vals, const uint32_t* starts,
-                           const uint32_t* d_nseg, uint64_t n_entries, uint32_t dim,
-                           const GradSource& grads, float* weights, float* state,
+                           const uint32_t* d_lo, const uint32_t* d_hi, uint64_t n_entries,
+                           uint32_t dim, const GradSource& grads, float* weights, float* state,
                            const OptParams& opt, const DenseRange& dense0,
                            const DenseRange& dense1, const SegmentScratch& sc,
                            cudaStream_t stream) {
@@ -553,9 +575,9 @@ void launch_segment_update(const uint32_t* keys, const uint32_t* vals, const uin
   const unsigned grid = persistent_grid(8);
   dispatch_dim(dim, [&](auto D) {
     constexpr int DIM = decltype(D)::value;
-    seg_short_kernel<DIM><<<grid, kThreads, 0, stream>>>(keys, vals, starts, d_nseg, grads, weights,
-                                                         state, opt, dense0, dense1, sc.long_list,
-                                                         sc.long_count);
+    seg_short_kernel<DIM><<<grid, kThreads, 0, stream>>>(keys, vals, starts, d_lo, d_hi, grads,
+                                                         weights, state, opt, dense0, dense1,
+                                                         sc.long_list, sc.long_count);
     TSD_LAUNCH_CHECK();
     long_prefix_kernel<<<1, 1024, 0, stream>>>(sc.long_list, sc.long_count, starts, sc.piece_off);
     TSD_LAUNCH_CHECK();

@@ -70,12 +70,18 @@ struct SegmentScratch {
   uint32_t max_pieces = 0;
 };
 
+// Segments [*d_lo, *d_hi) (device scalars, so ranges can be chosen on the
+// device without a host sync).
 void launch_segment_update(const uint32_t* keys, const uint32_t* vals, const uint32_t* starts,
-                           const uint32_t* d_nseg, uint64_t n_entries, uint32_t dim,
-                           const GradSource& grads, float* weights, float* state,
+                           const uint32_t* d_lo, const uint32_t* d_hi, uint64_t n_entries,
+                           uint32_t dim, const GradSource& grads, float* weights, float* state,
                            const OptParams& opt, const DenseRange& dense0,
                            const DenseRange& dense1, const SegmentScratch& scratch,
                            cudaStream_t stream);
+
+// out[0] = 0, out[1] = number of segments whose key < split_key.
+void launch_segment_split(const uint32_t* keys, const uint32_t* starts, const uint32_t* d_nseg,
+                          uint32_t split_key, uint32_t* out, cudaStream_t stream);
 
 // Dense optimizer over rows [row_lo, row_lo + rows) with gradients g[rows x dim].
 void launch_dense_update(const float* grad, uint32_t rows, uint32_t row_lo, uint32_t dim,

@@ -94,7 +94,10 @@ const char* const kPhaseNames[kNumPhases] = {
 struct ts_table {
   ts_table_config cfg{};
   uint32_t U = 1, W = 1, N = 1, g = 0, slot = 0, node = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;  // compute stream (S)
+  cudaStream_t comm = nullptr;    // exchange / all-reduce stream (C), U > 1
+  cudaEvent_t ev_ids = nullptr, ev_fwd = nullptr, ev_bwd0 = nullptr, ev_grads = nullptr,
+              ev_dense = nullptr, ev_ar = nullptr;
   ncclComm_t world = nullptr, intra = nullptr, cross = nullptr;
 
   // shard
@@ -118,7 +121,7 @@ struct ts_table {
   // dedup / sort
   tsd::DevBuf<uint32_t> keys_a, vals_a, keys_b, vals_b, ghist, goff, sort_counters;
   tsd::DevBuf<uint64_t> sort_status;
-  tsd::DevBuf<uint32_t> starts, seg_scratch, nseg;
+  tsd::DevBuf<uint32_t> starts, seg_scratch, nseg, seg_split;
   tsd::DevBuf<uint32_t> long_list, long_count, piece_off, entry_keys, entry_vals;
   tsd::DevBuf<float> partials;
   // U > 1 routing / exchange
@@ -134,14 +137,16 @@ struct ts_table {
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
   std::vector<std::pair<int, int>> ev_used;  // (phase, pool index)
+  std::vector<cudaStream_t> ev_stream;        // stream of each used pair
   double phase_ms[tsd::kNumPhases] = {};
   uint64_t phase_launches[tsd::kNumPhases] = {};
 
   uint32_t nb() const { return U + W + 1; }  // buckets incl. the local one
 
   // --- timing helpers --------------------------------------------------------
-  int phase_begin(int phase) {
+  int phase_begin(int phase, cudaStream_t on = nullptr) {
     if (!timing) return -1;
+    if (!on) on = stream;
     const size_t idx = ev_used.size();
     if (idx >= ev_pool.size()) {
       cudaEvent_t a, b;
@@ -149,17 +154,20 @@ struct ts_table {
       TSD_CUDA(cudaEventCreate(&b));
       ev_pool.emplace_back(a, b);
     }
-    TSD_CUDA(cudaEventRecord(ev_pool[idx].first, stream));
+    TSD_CUDA(cudaEventRecord(ev_pool[idx].first, on));
     ev_used.emplace_back(phase, static_cast<int>(idx));
+    ev_stream.push_back(on);
     return static_cast<int>(idx);
   }
   void phase_end(int token) {
     if (token < 0) return;
-    TSD_CUDA(cudaEventRecord(ev_pool[token].second, stream));
+    TSD_CUDA(cudaEventRecord(ev_pool[token].second, ev_stream[token]));
   }
   void collect_timing() {
     if (ev_used.empty()) return;
     TSD_CUDA(cudaStreamSynchronize(stream));
+    if (comm) TSD_CUDA(cudaStreamSynchronize(comm));
+    ev_stream.clear();
     for (const auto& [phase, idx] : ev_used) {
       float ms = 0.f;
       TSD_CUDA(cudaEventElapsedTime(&ms, ev_pool[idx].first, ev_pool[idx].second));
@@ -206,7 +214,7 @@ struct ts_table {
   void exchange(const void* send, const std::vector<uint64_t>& s_off,
                 const std::vector<uint64_t>& s_cnt, void* recv,
                 const std::vector<uint64_t>& r_off, const std::vector<uint64_t>& r_cnt,
-                size_t elem_bytes, bool flex_part_only_intra);
+                size_t elem_bytes, cudaStream_t on);
   void destroy();
 };
 
@@ -304,6 +312,7 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
   d_loss.ensure(1);
   tier_counts.ensure(4);
   nseg.ensure(4);
+  seg_split.ensure(4);
   long_count.ensure(4);
   ensure_sort_capacity(c.max_occurrences);
   if (U > 1) {
@@ -316,6 +325,10 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     dense_dp.ensure(std::max<uint64_t>(dp_rows, 1) * c.dim);
     if (N > 1) dense_flex.ensure(std::max<uint64_t>(flex_rows, 1) * c.dim);
     // communicators: world, intra (color = node), cross (color = slot)
+    TSD_CUDA(cudaStreamCreateWithFlags(&comm, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&ev_ids, &ev_fwd, &ev_bwd0, &ev_grads, &ev_dense, &ev_ar}) {
+      TSD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
     ncclUniqueId id;
     std::memcpy(&id, c.nccl_unique_id, sizeof(id));
     TSD_NCCL(ncclCommInitRank(&world, static_cast<int>(U), id, static_cast<int>(g)));
@@ -333,7 +346,7 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
 void ts_table::exchange(const void* send, const std::vector<uint64_t>& s_off,
                         const std::vector<uint64_t>& s_cnt, void* recv,
                         const std::vector<uint64_t>& r_off, const std::vector<uint64_t>& r_cnt,
-                        size_t elem_bytes, bool /*unused*/) {
+                        size_t elem_bytes, cudaStream_t on) {
   // s_off/s_cnt/r_off/r_cnt have 2*U entries: [p*2 + 0] RW, [p*2 + 1] Flex.
   auto* sb = static_cast<const char*>(send);
   auto* rb = static_cast<char*>(recv);
@@ -341,15 +354,15 @@ void ts_table::exchange(const void* send, const std::vector<uint64_t>& s_off,
   for (uint32_t p = 0; p < U; ++p) {
     if (p == g) continue;
     const size_t s0 = s_cnt[2 * p] * elem_bytes, r0 = r_cnt[2 * p] * elem_bytes;
-    if (s0) TSD_NCCL(ncclSend(sb + s_off[2 * p] * elem_bytes, s0, ncclChar, static_cast<int>(p), world, stream));
-    if (r0) TSD_NCCL(ncclRecv(rb + r_off[2 * p] * elem_bytes, r0, ncclChar, static_cast<int>(p), world, stream));
+    if (s0) TSD_NCCL(ncclSend(sb + s_off[2 * p] * elem_bytes, s0, ncclChar, static_cast<int>(p), world, on));
+    if (r0) TSD_NCCL(ncclRecv(rb + r_off[2 * p] * elem_bytes, r0, ncclChar, static_cast<int>(p), world, on));
   }
   for (uint32_t p = node * W; p < (node + 1) * W; ++p) {
     if (p == g) continue;
     const int peer = static_cast<int>(p % W);  // rank inside the intra comm
     const size_t s1 = s_cnt[2 * p + 1] * elem_bytes, r1 = r_cnt[2 * p + 1] * elem_bytes;
-    if (s1) TSD_NCCL(ncclSend(sb + s_off[2 * p + 1] * elem_bytes, s1, ncclChar, peer, intra, stream));
-    if (r1) TSD_NCCL(ncclRecv(rb + r_off[2 * p + 1] * elem_bytes, r1, ncclChar, peer, intra, stream));
+    if (s1) TSD_NCCL(ncclSend(sb + s_off[2 * p + 1] * elem_bytes, s1, ncclChar, peer, intra, on));
+    if (r1) TSD_NCCL(ncclRecv(rb + r_off[2 * p + 1] * elem_bytes, r1, ncclChar, peer, intra, on));
   }
   TSD_NCCL(ncclGroupEnd());
 }
@@ -404,11 +417,14 @@ void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
     // single counting pass: its global digit offsets ARE the bucket starts
     launch_bucket_starts(goff.ptr, 1, nb(), static_cast<uint32_t>(occ),
                          bucket_start.ptr, stream);
-    TSD_NCCL(ncclAllGather(bucket_start.ptr, all_counts.ptr, nb() + 1, ncclUint32, world, stream));
+    // every NCCL call of this table is issued on the comm stream
+    TSD_CUDA(cudaEventRecord(ev_ids, stream));
+    TSD_CUDA(cudaStreamWaitEvent(comm, ev_ids, 0));
+    TSD_NCCL(ncclAllGather(bucket_start.ptr, all_counts.ptr, nb() + 1, ncclUint32, world, comm));
     h_counts.resize(static_cast<size_t>(U) * (nb() + 1));
     TSD_CUDA(cudaMemcpyAsync(h_counts.data(), all_counts.ptr, sizeof(uint32_t) * U * (nb() + 1),
-                             cudaMemcpyDeviceToHost, stream));
-    TSD_CUDA(cudaStreamSynchronize(stream));
+                             cudaMemcpyDeviceToHost, comm));
+    TSD_CUDA(cudaStreamSynchronize(comm));
   }
   // Send layout: my remote buckets are contiguous in bucket order (RW by
   // server, then Flex by slot); receive layout is ordered by source rank
@@ -427,28 +443,28 @@ void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   recv_ids.ensure(recv_total);
   recv_rows.ensure(recv_total * cfg.dim);
 
-  // ---- ids of remote occurrences, exchange ---------------------------------
+  // ---- exchange chain on the comm stream, local gather on the compute
+  // stream: the NVLink all-to-allv overlaps the HBM-bound local gather ------
   launch_remote_ids(d_rows, order.ptr, n_remote, d_local, send_ids.ptr, stream);
-  t = phase_begin(kPhaseExchangeFwd);
-  exchange(send_ids.ptr, send_off, send_cnt, recv_ids.ptr, recv_off, recv_cnt, sizeof(uint32_t), false);
+  TSD_CUDA(cudaEventRecord(ev_ids, stream));
+  TSD_CUDA(cudaStreamWaitEvent(comm, ev_ids, 0));
+  t = phase_begin(kPhaseExchangeFwd, comm);
+  exchange(send_ids.ptr, send_off, send_cnt, recv_ids.ptr, recv_off, recv_cnt, sizeof(uint32_t), comm);
+  // server side: rows requested by peers, in received order
+  launch_copy_rows(d_w, recv_ids.ptr, recv_rows.ptr, nullptr, recv_total, cfg.dim, comm);
+  exchange(recv_rows.ptr, recv_off, recv_cnt, send_rows.ptr, send_off, send_cnt,
+           sizeof(float) * cfg.dim, comm);
   phase_end(t);
+  t = phase_begin(kPhaseScatter, comm);
+  launch_scatter_rows_loss(send_rows.ptr, d_out, order.ptr, n_remote, cfg.dim,
+                           loss_partials.ptr + gather_grid, gather_grid, comm);
+  phase_end(t);
+  TSD_CUDA(cudaEventRecord(ev_fwd, comm));
 
-  // ---- local gather (DP + own shard) ---------------------------------------
   t = phase_begin(kPhaseGather);
   launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, gather_grid, stream);
-  // server side: rows requested by peers, in received order
-  launch_copy_rows(d_w, recv_ids.ptr, recv_rows.ptr, nullptr, recv_total, cfg.dim, stream);
   phase_end(t);
-
-  // ---- rows back to requesters ---------------------------------------------
-  t = phase_begin(kPhaseExchangeFwd);
-  exchange(recv_rows.ptr, recv_off, recv_cnt, send_rows.ptr, send_off, send_cnt,
-           sizeof(float) * cfg.dim, false);
-  phase_end(t);
-  t = phase_begin(kPhaseScatter);
-  launch_scatter_rows_loss(send_rows.ptr, d_out, order.ptr, n_remote, cfg.dim,
-                           loss_partials.ptr + gather_grid, gather_grid, stream);
-  phase_end(t);
+  TSD_CUDA(cudaStreamWaitEvent(stream, ev_fwd, 0));
   // loss = local-gather partials + scatter partials, fixed order
   launch_loss_finalize(loss_partials.ptr, 2 * gather_grid, d_loss.ptr, stream);
 }
@@ -470,93 +486,119 @@ void ts_table::backward(const float* d_grad) {
   GradSource gs;
   gs.local = d_grad;
   gs.n_local = static_cast<uint32_t>(occ);
-
-  const uint32_t* keys_in = nullptr;
-  const uint32_t* vals_in = nullptr;
-  uint64_t m = occ;
-  if (U == 1) {
-    keys_in = last_rows;  // local id == canonical index; vals = iota
-  } else {
-    // grads of remote occurrences -> servers (reverse of the row exchange)
-    int t = phase_begin(kPhaseExchangeBwd);
-    launch_copy_rows(d_grad, order.ptr, send_rows.ptr, nullptr, n_remote, cfg.dim, stream);
-    exchange(send_rows.ptr, send_off, send_cnt, recv_rows.ptr, recv_off, recv_cnt,
-             sizeof(float) * cfg.dim, false);
-    phase_end(t);
-    gs.remote = recv_rows.ptr;
-    m = n_local_occ + recv_total;
-    entry_keys.ensure(m);
-    entry_vals.ensure(m);
-    ensure_sort_capacity(m);
-    launch_build_entries(last_rows, order.ptr + n_remote, n_local_occ, rv, recv_ids.ptr, recv_before,
-                         recv_total, static_cast<uint32_t>(occ), entry_keys.ptr, entry_vals.ptr,
-                         stream);
-    keys_in = entry_keys.ptr;
-    vals_in = entry_vals.ptr;
-    if (dp_rows) {
-      d0.lo = 0;
-      d0.hi = static_cast<uint32_t>(dp_rows);
-      d0.grad = dense_dp.ptr;
-      TSD_CUDA(cudaMemsetAsync(dense_dp.ptr, 0, sizeof(float) * dp_rows * cfg.dim, stream));
-    }
-    if (N > 1 && flex_rows) {
-      d1.lo = static_cast<uint32_t>(dp_rows);
-      d1.hi = static_cast<uint32_t>(dp_rows + flex_rows);
-      d1.grad = dense_flex.ptr;
-      TSD_CUDA(cudaMemsetAsync(dense_flex.ptr, 0, sizeof(float) * flex_rows * cfg.dim, stream));
-    }
-  }
-  last_entries = m;
-
-  int t = phase_begin(kPhaseSort);
-  RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, ghist.ptr, goff.ptr,
-                  sort_status.ptr, sort_counters.ptr};
-  uint32_t* sk = nullptr;
-  uint32_t* sv = nullptr;
-  radix_sort_pairs(keys_in, vals_in, m, bits_for(local_rows ? local_rows - 1 : 0), rb, &sk, &sv, stream);
-  phase_end(t);
-  t = phase_begin(kPhaseSegments);
-  segment_starts(sk, m, starts.ptr, nseg.ptr, seg_scratch.ptr, stream);
-  phase_end(t);
-  t = phase_begin(kPhaseSegmentUpdate);
   SegmentScratch sc;
   sc.long_list = long_list.ptr;
   sc.long_count = long_count.ptr;
   sc.piece_off = piece_off.ptr;
   sc.partials = partials.ptr;
-  launch_segment_update(sk, sv, starts.ptr, nseg.ptr, m, cfg.dim, gs, d_w, d_state, opt, d0, d1, sc,
-                        stream);
-  phase_end(t);
+  RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, ghist.ptr, goff.ptr,
+                  sort_status.ptr, sort_counters.ptr};
+  uint32_t* sk = nullptr;
+  uint32_t* sv = nullptr;
+  const int key_bits = bits_for(local_rows ? local_rows - 1 : 0);
 
-  if (U > 1) {
-    t = phase_begin(kPhaseAllReduce);
-    TSD_NCCL(ncclGroupStart());
-    if (dp_rows) {
-      TSD_NCCL(ncclAllReduce(dense_dp.ptr, dense_dp.ptr, dp_rows * cfg.dim, ncclFloat32, ncclSum, world,
-                             stream));
-    }
-    if (N > 1 && flex_rows) {
-      TSD_NCCL(ncclAllReduce(dense_flex.ptr, dense_flex.ptr, flex_rows * cfg.dim, ncclFloat32, ncclSum,
-                             cross, stream));
-    }
-    TSD_NCCL(ncclGroupEnd());
+  if (U == 1) {
+    // local id == canonical index: sort the forward's rows directly
+    last_entries = occ;
+    int t = phase_begin(kPhaseSort);
+    radix_sort_pairs(last_rows, nullptr, occ, key_bits, rb, &sk, &sv, stream);
     phase_end(t);
-    t = phase_begin(kPhaseDenseUpdate);
-    if (dp_rows) {
-      launch_dense_update(dense_dp.ptr, static_cast<uint32_t>(dp_rows), 0, cfg.dim, d_w, d_state, opt,
-                          stream);
-    }
-    if (N > 1 && flex_rows) {
-      launch_dense_update(dense_flex.ptr, static_cast<uint32_t>(flex_rows),
-                          static_cast<uint32_t>(dp_rows), cfg.dim, d_w, d_state, opt, stream);
-    }
+    t = phase_begin(kPhaseSegments);
+    segment_starts(sk, occ, starts.ptr, nseg.ptr, seg_scratch.ptr, stream);
+    launch_segment_split(sk, starts.ptr, nseg.ptr, 0u, seg_split.ptr, stream);  // [0] = 0
     phase_end(t);
+    t = phase_begin(kPhaseSegmentUpdate);
+    launch_segment_update(sk, sv, starts.ptr, seg_split.ptr, nseg.ptr, occ, cfg.dim, gs, d_w, d_state,
+                          opt, d0, d1, sc, stream);
+    phase_end(t);
+    return;
   }
+
+  // ---- comm stream: grads of remote occurrences -> their servers ------------
+  TSD_CUDA(cudaEventRecord(ev_bwd0, stream));
+  TSD_CUDA(cudaStreamWaitEvent(comm, ev_bwd0, 0));
+  int t = phase_begin(kPhaseExchangeBwd, comm);
+  launch_copy_rows(d_grad, order.ptr, send_rows.ptr, nullptr, n_remote, cfg.dim, comm);
+  exchange(send_rows.ptr, send_off, send_cnt, recv_rows.ptr, recv_off, recv_cnt,
+           sizeof(float) * cfg.dim, comm);
+  phase_end(t);
+  TSD_CUDA(cudaEventRecord(ev_grads, comm));
+
+  // ---- compute stream, overlapped: keys/values need only ids, not grads ----
+  gs.remote = recv_rows.ptr;
+  const uint64_t m = n_local_occ + recv_total;
+  last_entries = m;
+  entry_keys.ensure(m);
+  entry_vals.ensure(m);
+  ensure_sort_capacity(m);
+  rb = RadixBuffers{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, ghist.ptr, goff.ptr,
+                    sort_status.ptr, sort_counters.ptr};
+  sc.long_list = long_list.ptr;
+  sc.piece_off = piece_off.ptr;
+  sc.partials = partials.ptr;
+  launch_build_entries(last_rows, order.ptr + n_remote, n_local_occ, rv, recv_ids.ptr, recv_before,
+                       recv_total, static_cast<uint32_t>(occ), entry_keys.ptr, entry_vals.ptr, stream);
+  // replicated tiers reduce into dense buffers: DP always, Flex across nodes
+  if (dp_rows) {
+    d0 = DenseRange{0, static_cast<uint32_t>(dp_rows), dense_dp.ptr};
+    TSD_CUDA(cudaMemsetAsync(dense_dp.ptr, 0, sizeof(float) * dp_rows * cfg.dim, stream));
+  }
+  if (N > 1 && flex_rows) {
+    d1 = DenseRange{static_cast<uint32_t>(dp_rows), static_cast<uint32_t>(dp_rows + flex_rows),
+                    dense_flex.ptr};
+    TSD_CUDA(cudaMemsetAsync(dense_flex.ptr, 0, sizeof(float) * flex_rows * cfg.dim, stream));
+  }
+  t = phase_begin(kPhaseSort);
+  radix_sort_pairs(entry_keys.ptr, entry_vals.ptr, m, key_bits, rb, &sk, &sv, stream);
+  phase_end(t);
+  t = phase_begin(kPhaseSegments);
+  segment_starts(sk, m, starts.ptr, nseg.ptr, seg_scratch.ptr, stream);
+  // dense-reduced rows are the lowest local ids: split the segments there
+  const uint32_t dense_hi = static_cast<uint32_t>(dp_rows + (N > 1 ? flex_rows : 0));
+  launch_segment_split(sk, starts.ptr, nseg.ptr, dense_hi, seg_split.ptr, stream);
+  phase_end(t);
+  TSD_CUDA(cudaStreamWaitEvent(stream, ev_grads, 0));
+
+  // ---- replicated rows first; their all-reduce overlaps the RW updates ----
+  t = phase_begin(kPhaseSegmentUpdate);
+  launch_segment_update(sk, sv, starts.ptr, seg_split.ptr, seg_split.ptr + 1, m, cfg.dim, gs, d_w,
+                        d_state, opt, d0, d1, sc, stream);
+  phase_end(t);
+  TSD_CUDA(cudaEventRecord(ev_dense, stream));
+  TSD_CUDA(cudaStreamWaitEvent(comm, ev_dense, 0));
+  t = phase_begin(kPhaseAllReduce, comm);
+  TSD_NCCL(ncclGroupStart());
+  if (dp_rows) {
+    TSD_NCCL(ncclAllReduce(dense_dp.ptr, dense_dp.ptr, dp_rows * cfg.dim, ncclFloat32, ncclSum, world, comm));
+  }
+  if (N > 1 && flex_rows) {
+    TSD_NCCL(ncclAllReduce(dense_flex.ptr, dense_flex.ptr, flex_rows * cfg.dim, ncclFloat32, ncclSum,
+                           cross, comm));
+  }
+  TSD_NCCL(ncclGroupEnd());
+  phase_end(t);
+  TSD_CUDA(cudaEventRecord(ev_ar, comm));
+
+  t = phase_begin(kPhaseSegmentUpdate);
+  launch_segment_update(sk, sv, starts.ptr, seg_split.ptr + 1, nseg.ptr, m, cfg.dim, gs, d_w, d_state,
+                        opt, d0, d1, sc, stream);
+  phase_end(t);
+  TSD_CUDA(cudaStreamWaitEvent(stream, ev_ar, 0));
+  t = phase_begin(kPhaseDenseUpdate);
+  if (dp_rows) {
+    launch_dense_update(dense_dp.ptr, static_cast<uint32_t>(dp_rows), 0, cfg.dim, d_w, d_state, opt, stream);
+  }
+  if (N > 1 && flex_rows) {
+    launch_dense_update(dense_flex.ptr, static_cast<uint32_t>(flex_rows), static_cast<uint32_t>(dp_rows),
+                        cfg.dim, d_w, d_state, opt, stream);
+  }
+  phase_end(t);
 }
 
 void ts_table::destroy() {
   cudaSetDevice(cfg.device);
   if (stream) cudaStreamSynchronize(stream);
+  if (comm) cudaStreamSynchronize(comm);
   if (world) ncclCommDestroy(world);
   if (intra) ncclCommDestroy(intra);
   if (cross) ncclCommDestroy(cross);
@@ -569,6 +611,7 @@ void ts_table::destroy() {
   tier_counts.release();
   rows_dev.release();
   sort_status.release();
+  seg_split.release();
   for (auto* b : {&keys_a, &vals_a, &keys_b, &vals_b, &ghist, &goff, &sort_counters, &starts,
                   &seg_scratch, &nseg, &long_list, &long_count, &piece_off, &entry_keys,
                   &entry_vals, &bucket, &order, &send_ids, &recv_ids, &bucket_start, &all_counts}) {
@@ -579,6 +622,10 @@ void ts_table::destroy() {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
   }
+  for (cudaEvent_t e : {ev_ids, ev_fwd, ev_bwd0, ev_grads, ev_dense, ev_ar}) {
+    if (e) cudaEventDestroy(e);
+  }
+  if (comm) cudaStreamDestroy(comm);
   if (stream) cudaStreamDestroy(stream);
 }
 
