@@ -333,6 +333,8 @@ def run_ours(args, dist: Dist):
     for k in range(prof_steps):
         step(k)
     phases = table.phase_times()
+    step(prof_steps)  # one more step: its timeline (both streams)
+    trace = [(n, sid, round(a, 4), round(b, 4)) for n, sid, a, b in table.phase_trace()]
     table.enable_timing(False)
 
     # ---- end to end through the host-buffer public entry point -------------
@@ -440,6 +442,7 @@ def run_ours(args, dist: Dist):
         "roofline": roofline,
         "a2a": a2a,
         "loss_last_step": loss,
+        "step_trace_ms": trace,
         "wall_s_timed": round(wall, 4),
         "prep_wall_s": doc.get("prep_wall_s"),
     }

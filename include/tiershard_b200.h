@@ -221,6 +221,11 @@ ts_status ts_table_enable_timing(ts_table* t, int enable);
 ts_status ts_table_phase_times(ts_table* t, double* ms, uint64_t* launches,
                                int capacity, int* count);
 const char* ts_table_phase_name(int phase);
+/* Timeline of the phases recorded since the last collection (timing must be
+ * enabled): phase index, stream (0 compute, 1 exchange), start / end in ms
+ * from the first recorded event.  Synchronises the table's streams. */
+ts_status ts_table_phase_trace(ts_table* t, int* phase, int* stream_id, double* t0_ms,
+                               double* t1_ms, int capacity, int* count);
 
 #ifdef __cplusplus
 }

@@ -67,6 +67,7 @@ EXPORTS = (
     "ts_table_enable_timing",
     "ts_table_phase_times",
     "ts_table_phase_name",
+    "ts_table_phase_trace",
 )
 
 
@@ -148,6 +149,7 @@ def load() -> C.CDLL:
         "ts_table_enable_timing": (C.c_int, [vp, C.c_int]),
         "ts_table_phase_times": (C.c_int, [vp, f64p, u64p, C.c_int, C.POINTER(C.c_int)]),
         "ts_table_phase_name": (C.c_char_p, [C.c_int]),
+        "ts_table_phase_trace": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.POINTER(C.c_int)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -332,6 +334,20 @@ class Table:
         return {
             self._lib.ts_table_phase_name(i).decode(): (ms[i], n_launch[i]) for i in range(count.value)
         }
+
+    def phase_trace(self) -> list:
+        """[(phase name, stream id, t0 ms, t1 ms)] of the last collected window."""
+        cap = 4096
+        ph = np.zeros(cap, np.int32)
+        sid = np.zeros(cap, np.int32)
+        t0 = np.zeros(cap, np.float64)
+        t1 = np.zeros(cap, np.float64)
+        count = C.c_int(0)
+        _check(self._lib.ts_table_phase_trace(self._h, _ptr(ph), _ptr(sid), _ptr(t0), _ptr(t1), cap,
+                                              C.byref(count)))
+        n = min(cap, count.value)
+        return [(self._lib.ts_table_phase_name(int(ph[i])).decode(), int(sid[i]), float(t0[i]), float(t1[i]))
+                for i in range(n)]
 
     def close(self):
         if getattr(self, "_h", None):

@@ -166,8 +166,12 @@ loss_finalize_kernel(const double* __restrict__ partials, unsigned count, double
 
 template <int VEC>
 __device__ __forceinline__ const float* grad_row(const GradSource& gs, uint32_t v, uint32_t dim) {
-  return v < gs.n_local ? gs.local + static_cast<uint64_t>(v) * dim
-                        : gs.remote + static_cast<uint64_t>(v - gs.n_local) * dim;
+  if (v < gs.n_local) return gs.local + static_cast<uint64_t>(v) * dim;
+  const uint32_t r = v - gs.n_local;
+  if (gs.remote) return gs.remote + static_cast<uint64_t>(r) * dim;
+  int s = 0;  // source rank of received entry r (<= 8 ranges)
+  while (s + 1 < gs.npeer && r >= gs.src_start[s + 1]) ++s;
+  return gs.peer[s] + static_cast<uint64_t>(__ldg(gs.recv_pos + r)) * dim;
 }
 
 // Finishes one reduced row: dense-range rows park their gradient, others get
@@ -488,6 +492,63 @@ dense_update_kernel(const float* __restrict__ grad, uint32_t rows, uint32_t row_
   }
 }
 
+template <int DIM>
+__global__ void __launch_bounds__(kThreads)
+replica_update_kernel(ReplicaGroup grp, OptParams opt) {
+  constexpr int VEC = DIM / 32;
+  constexpr int R = DIM <= 128 ? 4 : 1;  // rows in flight per warp (peer latency)
+  const unsigned lane = threadIdx.x & 31u;
+  const uint32_t per = (grp.rows + grp.size - 1) / grp.size;
+  const uint32_t lo = per * grp.me;
+  const uint32_t hi = min(grp.rows, lo + per);
+  const uint32_t gwarp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
+  float* mine = grp.weights[grp.me];
+  float* my_state = grp.state[grp.me];
+  for (uint32_t r0 = lo + gwarp * R; r0 < hi; r0 += nwarps * R) {
+    float g[R][VEC];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      if (r0 + i >= hi) continue;
+      const uint64_t off = static_cast<uint64_t>(r0 + i) * DIM + lane * VEC;
+      float part[kMaxGradPeers][VEC];
+#pragma unroll
+      for (int k = 0; k < kMaxGradPeers; ++k) {  // all members' loads in flight
+        if (k < grp.size) load_lane<VEC>(grp.grads[k] + off, part[k]);
+      }
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) g[i][j] = part[0][j];
+#pragma unroll
+      for (int k = 1; k < kMaxGradPeers; ++k) {
+        if (k < grp.size) {
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) g[i][j] = __fadd_rn(g[i][j], part[k][j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const uint32_t r = r0 + i;
+      if (r >= hi) continue;
+      // optimizer on my replica, then broadcast the row (+ state) to the others
+      finish_row<DIM>(r, g[i], mine, my_state, opt, DenseRange{}, DenseRange{});
+      __syncwarp();
+      const uint64_t off = static_cast<uint64_t>(r) * DIM + lane * VEC;
+      float w[VEC];
+      load_lane<VEC>(mine + off, w);
+      const float st = my_state ? my_state[r] : 0.0f;
+#pragma unroll
+      for (int k = 0; k < kMaxGradPeers; ++k) {
+        if (k < grp.size && k != grp.me) {
+          store_lane<VEC>(grp.weights[k] + off, w);
+          if (my_state && lane == 0) grp.state[k][r] = st;
+        }
+      }
+    }
+  }
+  __threadfence_system();
+}
+
 __global__ void __launch_bounds__(kThreads)
 init_weights_kernel(float* __restrict__ weights, uint64_t local_rows, uint32_t dim, uint64_t seed,
                     const uint32_t* __restrict__ l2c) {
@@ -517,14 +578,22 @@ void dispatch_dim(uint32_t dim, F&& f) {
   }
 }
 
-unsigned persistent_grid(unsigned per_sm = 8) { return static_cast<unsigned>(sm_count()) * per_sm; }
+unsigned persistent_grid(unsigned per_sm) { return static_cast<unsigned>(sm_count()) * per_sm; }
+
+// Blocks per SM of the compute-stream persistent grids.  With U > 1 the table
+// lowers it so the exchange / replica kernels on the (high-priority) comm
+// stream always find free SM slots instead of queueing behind grids that
+// never retire a block (one table per process, set at creation).
+unsigned g_compute_blocks_per_sm = 8;
 
 }  // namespace
 
 unsigned gather_grid(uint64_t occ) {
   const uint64_t want = (occ + 63) / 64;
-  return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, persistent_grid(8))));
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, persistent_grid(g_compute_blocks_per_sm))));
 }
+
+void set_compute_blocks_per_sm(unsigned per_sm) { g_compute_blocks_per_sm = per_sm; }
 
 void launch_gather_local(const uint32_t* rows, uint64_t occ, const float* weights, float* out,
                          const RemapView& remap, uint32_t dim, double* loss_partials,
@@ -572,7 +641,7 @@ void launch_segment_update(const uint32_t* keys, const uint32_t* vals, const uin
                            cudaStream_t stream) {
   if (n_entries == 0) return;
   TSD_CUDA(cudaMemsetAsync(sc.long_count, 0, sizeof(uint32_t), stream));
-  const unsigned grid = persistent_grid(8);
+  const unsigned grid = persistent_grid(g_compute_blocks_per_sm);
   dispatch_dim(dim, [&](auto D) {
     constexpr int DIM = decltype(D)::value;
     seg_short_kernel<DIM><<<grid, kThreads, 0, stream>>>(keys, vals, starts, d_lo, d_hi, grads,
@@ -599,6 +668,19 @@ void launch_dense_update(const float* grad, uint32_t rows, uint32_t row_lo, uint
   dispatch_dim(dim, [&](auto D) {
     constexpr int DIM = decltype(D)::value;
     dense_update_kernel<DIM><<<grid, kThreads, 0, stream>>>(grad, rows, row_lo, weights, state, opt);
+  });
+  TSD_LAUNCH_CHECK();
+}
+
+void launch_replica_update(const ReplicaGroup& grp, uint32_t dim, const OptParams& opt,
+                           cudaStream_t stream) {
+  if (grp.rows == 0 || grp.size == 0) return;
+  const uint32_t per = (grp.rows + grp.size - 1) / grp.size;
+  const unsigned grid = std::max<unsigned>(
+      1, std::min<unsigned>(persistent_grid(g_compute_blocks_per_sm), ceil_div(per, kThreads / 32)));
+  dispatch_dim(dim, [&](auto D) {
+    constexpr int DIM = decltype(D)::value;
+    replica_update_kernel<DIM><<<grid, kThreads, 0, stream>>>(grp, opt);
   });
   TSD_LAUNCH_CHECK();
 }

@@ -36,12 +36,21 @@ struct DenseRange {
   float* grad = nullptr;
 };
 
+constexpr int kMaxGradPeers = 8;
+
 // Gradient source of sorted entry value v: v < n_local -> local grads
-// [n_local x dim], else remote grads [(v - n_local) x dim].
+// [n_local x dim]; else r = v - n_local is a received entry: staged mode
+// reads remote[r x dim]; peer mode (remote == nullptr) reads the row straight
+// from the requesting rank's gradient buffer over NVLink:
+// peer[s][recv_pos[r] x dim] with s the source whose recv range holds r.
 struct GradSource {
   const float* local = nullptr;
   const float* remote = nullptr;
   uint32_t n_local = 0;
+  const uint32_t* recv_pos = nullptr;
+  const float* peer[kMaxGradPeers] = {};
+  uint32_t src_start[kMaxGradPeers + 1] = {};
+  int npeer = 0;
 };
 
 // out[i] = W[local(rows[i])] for every occurrence served locally; remote
@@ -51,6 +60,9 @@ void launch_gather_local(const uint32_t* rows, uint64_t occ, const float* weight
                          const RemapView& remap, uint32_t dim, double* loss_partials,
                          unsigned grid, cudaStream_t stream);
 unsigned gather_grid(uint64_t occ);
+// Blocks per SM of the compute-stream persistent grids (8 = whole SM; the
+// table sets 6 when U > 1 so comm-stream kernels keep two slots per SM).
+void set_compute_blocks_per_sm(unsigned per_sm);
 
 // Final fixed-order reduction of the loss partials: *loss = 0.5 * sum.
 void launch_loss_finalize(const double* partials, unsigned count, double* loss,
@@ -86,6 +98,26 @@ void launch_segment_split(const uint32_t* keys, const uint32_t* starts, const ui
 // Dense optimizer over rows [row_lo, row_lo + rows) with gradients g[rows x dim].
 void launch_dense_update(const float* grad, uint32_t rows, uint32_t row_lo, uint32_t dim,
                          float* weights, float* state, const OptParams& opt, cudaStream_t stream);
+
+// Replicated-tier update over peer memory (replaces all-reduce + dense
+// update): the `size` ranks of a replica group each own a contiguous slice of
+// the group's dense rows; for each owned row the owner sums the members'
+// partial gradients grads[0..size) IN GROUP-RANK ORDER (peer loads), applies
+// the optimizer to its replica and stores the updated row (and Adagrad state)
+// into every member's replica (peer stores).  Deterministic and identical on
+// all replicas by construction.
+struct ReplicaGroup {
+  int size = 0;
+  int me = 0;                              // my index in the group
+  const float* grads[kMaxGradPeers] = {};  // dense partials [rows x dim], by group rank
+  float* weights[kMaxGradPeers] = {};      // replicas: weights + row_lo * dim
+  float* state[kMaxGradPeers] = {};        // Adagrad state + row_lo (may be null)
+  uint32_t rows = 0;                       // dense rows of the tier
+  uint32_t row_lo = 0;                     // local id of dense row 0
+};
+
+void launch_replica_update(const ReplicaGroup& grp, uint32_t dim, const OptParams& opt,
+                           cudaStream_t stream);
 
 // weights[l, d] = init_weight(seed, canon(l), d); canon = l when l2c == nullptr.
 void launch_init_weights(float* weights, uint64_t local_rows, uint32_t dim, uint64_t seed,

@@ -52,6 +52,17 @@ remote_ids_kernel(const uint32_t* __restrict__ rows, const uint32_t* __restrict_
   }
 }
 
+__global__ void __launch_bounds__(kThreads)
+remote_ids_upto_kernel(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ order,
+                       uint64_t max_count, const uint32_t* __restrict__ d_count,
+                       const uint32_t* __restrict__ local, uint32_t* __restrict__ ids) {
+  const uint64_t count = min(static_cast<uint64_t>(*d_count), max_count);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads;
+  for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x; j < count; j += stride) {
+    ids[j] = __ldg(local + __ldg(rows + __ldg(order + j)));
+  }
+}
+
 // One warp per row, float4 lanes; 4 rows in flight per warp.
 __global__ void __launch_bounds__(kThreads)
 copy_rows_kernel(const float* __restrict__ src, const uint32_t* __restrict__ src_idx,
@@ -170,6 +181,15 @@ void launch_remote_ids(const uint32_t* rows, const uint32_t* order, uint64_t cou
                        const uint32_t* local, uint32_t* ids, cudaStream_t stream) {
   if (count == 0) return;
   remote_ids_kernel<<<grid_for(count, kThreads * 4), kThreads, 0, stream>>>(rows, order, count, local, ids);
+  TSD_LAUNCH_CHECK();
+}
+
+void launch_remote_ids_upto(const uint32_t* rows, const uint32_t* order, uint64_t max_count,
+                            const uint32_t* d_count, const uint32_t* local, uint32_t* ids,
+                            cudaStream_t stream) {
+  if (max_count == 0) return;
+  remote_ids_upto_kernel<<<grid_for(max_count, kThreads * 4), kThreads, 0, stream>>>(rows, order, max_count,
+                                                                                   d_count, local, ids);
   TSD_LAUNCH_CHECK();
 }
 

@@ -30,6 +30,11 @@ void launch_bucket_keys(const uint32_t* rows, uint64_t occ, const BucketView& bv
 void launch_remote_ids(const uint32_t* rows, const uint32_t* order, uint64_t count,
                        const uint32_t* local, uint32_t* ids, cudaStream_t stream);
 
+// Same for j < *d_count (device scalar), launched for up to max_count.
+void launch_remote_ids_upto(const uint32_t* rows, const uint32_t* order, uint64_t max_count,
+                            const uint32_t* d_count, const uint32_t* local, uint32_t* ids,
+                            cudaStream_t stream);
+
 // dst[dst_idx ? dst_idx[j] : j] = src[src_idx ? src_idx[j] : j] for j < count
 // (rows of `dim` floats).
 void launch_copy_rows(const float* src, const uint32_t* src_idx, float* dst,

@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -34,6 +35,7 @@
 #include "embedding.cuh"
 #include "primitives.cuh"
 #include "layout.hpp"
+#include "peer.cuh"
 #include "route.cuh"
 
 namespace tsd {
@@ -81,12 +83,14 @@ enum Phase : int {
   kPhaseSegmentUpdate,
   kPhaseAllReduce,
   kPhaseDenseUpdate,
+  kPhaseReplicaUpdate,
   kNumPhases
 };
 
 const char* const kPhaseNames[kNumPhases] = {
     "route",         "gather",         "exchange_fwd", "scatter",  "exchange_bwd",
-    "dedup_sort",    "segment_starts", "segment_update", "allreduce", "dense_update"};
+    "dedup_sort",    "segment_starts", "segment_update", "allreduce", "dense_update",
+    "replica_update"};
 
 }  // namespace
 }  // namespace tsd
@@ -133,6 +137,35 @@ struct ts_table {
   uint64_t last_entries = 0;
   std::array<uint64_t, 3> last_tiers{};  // RW, Flex, DP (host, after sync)
 
+  // ---- peer-memory (NVLink P2P) exchange, U > 1 on one node ------------------
+  bool p2p = false;
+  tsd::PeerMappings peers;
+  tsd::DevBuf<uint32_t> recv_pos;
+  tsd::DevBuf<uint8_t> xfer;  // all-gather scratch [U x bytes]
+  tsd::DevBuf<int32_t> barrier_buf;
+  std::vector<uint8_t> h_xfer;
+  std::vector<const uint32_t*> peer_ids, peer_pos;  // peers' request lists (mapped)
+  std::vector<double*> peer_loss;                   // peers' remote-loss slots (mapped)
+  std::vector<const float*> peer_grad;              // peers' gradient buffers (mapped)
+  std::vector<const float*> peer_dense_dp, peer_dense_flex;  // peers' dense partials (mapped)
+  std::vector<float*> peer_w, peer_state;           // peers' shards (mapped)
+  tsd::IpcExport my_export{};                       // staging for the step payload
+  uint64_t remote_loss_slots = 0;                   // U * kServeGrid
+  // schedule knobs (env, read at creation; defaults = fastest measured):
+  //   TIERSHARD_REPLICA=serial|concurrent  replica update after the DP
+  //     segments on the compute stream, or on the comm stream beside the RW
+  //     segments;  TIERSHARD_PULL_GRADS=1|0  stage remote gradient rows into
+  //     HBM with one NVLink gather, or load them from peer memory in-kernel
+  bool replica_concurrent = true;
+  bool pull_grads = false;
+
+  size_t step_payload_bytes() const { return ((nb() + 1) * 4 + 7) / 8 * 8 + sizeof(tsd::IpcExport); }
+  std::vector<uint8_t> allgather_bytes(const void* mine, size_t bytes);
+  void barrier_on_comm();
+  void setup_p2p();
+  void forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out);
+  void backward_p2p(const float* d_grad);
+
   // timing
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
@@ -167,15 +200,28 @@ struct ts_table {
     if (ev_used.empty()) return;
     TSD_CUDA(cudaStreamSynchronize(stream));
     if (comm) TSD_CUDA(cudaStreamSynchronize(comm));
-    ev_stream.clear();
-    for (const auto& [phase, idx] : ev_used) {
-      float ms = 0.f;
+    // keep the timeline of the last step (offsets from its first event): a
+    // step starts at the first phase recorded after the previous collection
+    trace.clear();
+    const cudaEvent_t origin = ev_pool[ev_used.front().second].first;
+    for (size_t i = 0; i < ev_used.size(); ++i) {
+      const auto [phase, idx] = ev_used[i];
+      float ms = 0.f, t0 = 0.f, t1 = 0.f;
       TSD_CUDA(cudaEventElapsedTime(&ms, ev_pool[idx].first, ev_pool[idx].second));
+      TSD_CUDA(cudaEventElapsedTime(&t0, origin, ev_pool[idx].first));
+      TSD_CUDA(cudaEventElapsedTime(&t1, origin, ev_pool[idx].second));
       phase_ms[phase] += ms;
       phase_launches[phase] += 1;
+      trace.push_back({phase, ev_stream[i] == stream ? 0 : 1, t0, t1});
     }
+    ev_stream.clear();
     ev_used.clear();
   }
+  struct TraceRec {
+    int phase, stream_id;
+    float t0, t1;
+  };
+  std::vector<TraceRec> trace;  // timeline of the last collected window
 
   tsd::RemapView remap_view() const {
     tsd::RemapView rv;
@@ -308,7 +354,12 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
 
   // ---- step buffers ----------------------------------------------------------
   gather_grid = tsd::gather_grid(c.max_occurrences);
-  loss_partials.ensure(2 * gather_grid);
+  // [local gather partials | remote partials: staged scatter (gather_grid) or
+  //  peer servers' slots (U x kServeGrid)]; zeroed once — slots a server
+  //  never writes (our own) must read 0.
+  remote_loss_slots = static_cast<uint64_t>(U) * kServeGrid;
+  loss_partials.ensure(gather_grid + std::max<uint64_t>(gather_grid, remote_loss_slots));
+  TSD_CUDA(cudaMemsetAsync(loss_partials.ptr, 0, sizeof(double) * loss_partials.cap, stream));
   d_loss.ensure(1);
   tier_counts.ensure(4);
   nseg.ensure(4);
@@ -325,7 +376,12 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     dense_dp.ensure(std::max<uint64_t>(dp_rows, 1) * c.dim);
     if (N > 1) dense_flex.ensure(std::max<uint64_t>(flex_rows, 1) * c.dim);
     // communicators: world, intra (color = node), cross (color = slot)
-    TSD_CUDA(cudaStreamCreateWithFlags(&comm, cudaStreamNonBlocking));
+    // the exchange / replica stream gets the highest priority: its kernels
+    // are short, sit on the critical path, and would otherwise queue behind
+    // the persistent compute grids they overlap with
+    int lo_prio = 0, hi_prio = 0;
+    TSD_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    TSD_CUDA(cudaStreamCreateWithPriority(&comm, cudaStreamNonBlocking, hi_prio));
     for (cudaEvent_t* e : {&ev_ids, &ev_fwd, &ev_bwd0, &ev_grads, &ev_dense, &ev_ar}) {
       TSD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
@@ -334,7 +390,102 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     TSD_NCCL(ncclCommInitRank(&world, static_cast<int>(U), id, static_cast<int>(g)));
     TSD_NCCL(ncclCommSplit(world, static_cast<int>(node), static_cast<int>(g), &intra, nullptr));
     TSD_NCCL(ncclCommSplit(world, static_cast<int>(slot), static_cast<int>(g), &cross, nullptr));
+    setup_p2p();
   }
+}
+
+// All ranks contribute `bytes` bytes; returns the U x bytes concatenation.
+// Collective on the comm stream; synchronises it.
+std::vector<uint8_t> ts_table::allgather_bytes(const void* mine, size_t bytes) {
+  using namespace tsd;
+  xfer.ensure(bytes * U);
+  TSD_CUDA(cudaMemcpyAsync(xfer.ptr + bytes * g, mine, bytes, cudaMemcpyHostToDevice, comm));
+  TSD_NCCL(ncclAllGather(xfer.ptr + bytes * g, xfer.ptr, bytes, ncclUint8, world, comm));
+  std::vector<uint8_t> all(bytes * U);
+  TSD_CUDA(cudaMemcpyAsync(all.data(), xfer.ptr, bytes * U, cudaMemcpyDeviceToHost, comm));
+  TSD_CUDA(cudaStreamSynchronize(comm));
+  return all;
+}
+
+// Device-side rendezvous of all ranks on the comm stream (a 1-int all-reduce):
+// work queued before it on every rank completes before work queued after it.
+void ts_table::barrier_on_comm() {
+  using namespace tsd;
+  TSD_NCCL(ncclAllReduce(barrier_buf.ptr, barrier_buf.ptr, 1, ncclInt32, ncclSum, world, comm));
+}
+
+// Peer mode needs every pair of ranks to be NVLink/P2P reachable (one node)
+// and U <= 8; TIERSHARD_EXCHANGE=nccl forces the staged NCCL path.  The
+// decision is collective (min over ranks).
+void ts_table::setup_p2p() {
+  using namespace tsd;
+  barrier_buf.ensure(1);
+  TSD_CUDA(cudaMemsetAsync(barrier_buf.ptr, 0, sizeof(int32_t), comm));
+  int32_t ok = U <= kMaxPeerRanks && U <= kMaxGradPeers + 1 ? 1 : 0;
+  if (const char* env = std::getenv("TIERSHARD_EXCHANGE")) {
+    if (std::string(env) == "nccl") ok = 0;
+  }
+  char bus[32] = {};
+  TSD_CUDA(cudaDeviceGetPCIBusId(bus, sizeof(bus), cfg.device));
+  const std::vector<uint8_t> buses = allgather_bytes(bus, sizeof(bus));
+  for (uint32_t p = 0; p < U && ok; ++p) {
+    if (p == g) continue;
+    int dev = -1, can = 0;
+    if (cudaDeviceGetByPCIBusId(&dev, reinterpret_cast<const char*>(buses.data() + sizeof(bus) * p)) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+      break;
+    }
+    TSD_CUDA(cudaDeviceCanAccessPeer(&can, cfg.device, dev));
+    if (!can) ok = 0;
+  }
+  const std::vector<uint8_t> votes = allgather_bytes(&ok, sizeof(ok));
+  for (uint32_t p = 0; p < U; ++p) {
+    int32_t v;
+    std::memcpy(&v, votes.data() + sizeof(v) * p, sizeof(v));
+    if (!v) ok = 0;
+  }
+  p2p = ok != 0;
+  if (!p2p) return;
+  if (const char* env = std::getenv("TIERSHARD_REPLICA")) replica_concurrent = std::string(env) != "serial";
+  if (const char* env = std::getenv("TIERSHARD_PULL_GRADS")) pull_grads = std::string(env) == "1";
+  // export the table-owned buffers peers read or write
+  auto exp_or_none = [](const void* p) {
+    IpcExport e;
+    std::memset(&e, 0, sizeof(e));
+    return p ? export_pointer(p) : e;
+  };
+  constexpr int kExports = 7;
+  IpcExport mine[kExports] = {export_pointer(send_ids.ptr), export_pointer(order.ptr),
+                              export_pointer(loss_partials.ptr + gather_grid), exp_or_none(dense_dp.ptr),
+                              export_pointer(d_w), exp_or_none(d_state), exp_or_none(dense_flex.ptr)};
+  const std::vector<uint8_t> all = allgather_bytes(mine, sizeof(mine));
+  peer_ids.assign(U, nullptr);
+  peer_pos.assign(U, nullptr);
+  peer_loss.assign(U, nullptr);
+  peer_dense_dp.assign(U, nullptr);
+  peer_dense_flex.assign(U, nullptr);
+  peer_w.assign(U, d_w);
+  peer_state.assign(U, d_state);
+  peer_dense_dp[g] = dense_dp.ptr;
+  peer_dense_flex[g] = dense_flex.ptr;
+  for (uint32_t p = 0; p < U; ++p) {
+    if (p == g) continue;
+    IpcExport e[kExports];
+    std::memcpy(e, all.data() + sizeof(mine) * p, sizeof(mine));
+    const int pp = static_cast<int>(p);
+    auto open_opt = [&](const IpcExport& x) { return x.base_id ? peers.open(pp, x) : nullptr; };
+    peer_ids[p] = static_cast<const uint32_t*>(peers.open(pp, e[0]));
+    peer_pos[p] = static_cast<const uint32_t*>(peers.open(pp, e[1]));
+    peer_loss[p] = static_cast<double*>(peers.open(pp, e[2]));
+    peer_dense_dp[p] = static_cast<const float*>(open_opt(e[3]));
+    peer_w[p] = static_cast<float*>(peers.open(pp, e[4]));
+    peer_state[p] = static_cast<float*>(open_opt(e[5]));
+    peer_dense_flex[p] = static_cast<const float*>(open_opt(e[6]));
+  }
+  peer_grad.assign(U, nullptr);
+  xfer.ensure(step_payload_bytes() * U);
 }
 
 // ---------------------------------------------------------------------------
@@ -390,7 +541,12 @@ void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
     return;
   }
 
-  // ---- route: bucket + stable compaction of remote occurrences -------------
+  if (p2p) {
+    forward_p2p(d_rows, occ, d_out);
+    return;
+  }
+
+  // ---- staged NCCL path (no peer access): route, bucket, compaction -------
   int t = phase_begin(kPhaseRoute);
   BucketView bv;
   bv.dest = d_dest;
@@ -514,6 +670,11 @@ void ts_table::backward(const float* d_grad) {
     return;
   }
 
+  if (p2p) {
+    backward_p2p(d_grad);
+    return;
+  }
+
   // ---- comm stream: grads of remote occurrences -> their servers ------------
   TSD_CUDA(cudaEventRecord(ev_bwd0, stream));
   TSD_CUDA(cudaStreamWaitEvent(comm, ev_bwd0, 0));
@@ -593,6 +754,252 @@ void ts_table::backward(const float* d_grad) {
                         cfg.dim, d_w, d_state, opt, stream);
   }
   phase_end(t);
+}
+
+// ---------------------------------------------------------------------------
+// peer-memory forward / backward (U > 1, one node)
+// ---------------------------------------------------------------------------
+
+void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
+  using namespace tsd;
+  const RemapView rv = remap_view();
+  const size_t P = step_payload_bytes();
+  const size_t starts_bytes = P - sizeof(IpcExport);
+  uint8_t* my_slot = xfer.ptr + P * g;
+
+  // ---- route: bucket + one stable counting pass; request lists in HBM -----
+  int t = phase_begin(kPhaseRoute);
+  BucketView bv;
+  bv.dest = d_dest;
+  bv.dp_cut = cfg.dp_cut;
+  bv.flex_cut = cfg.flex_cut;
+  bv.u = U;
+  bv.w = W;
+  bv.rank = g;
+  bv.slot = slot;
+  launch_bucket_keys(d_rows, occ, bv, bucket.ptr, tier_counts.ptr, stream);
+  RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, ghist.ptr, goff.ptr,
+                  sort_status.ptr, sort_counters.ptr};
+  uint32_t* sorted_b = nullptr;
+  uint32_t* sorted_i = nullptr;
+  radix_sort_pairs(bucket.ptr, nullptr, occ, bits_for(nb() - 1), rb, &sorted_b, &sorted_i, stream);
+  TSD_CUDA(cudaMemcpyAsync(order.ptr, sorted_i, sizeof(uint32_t) * occ, cudaMemcpyDeviceToDevice, stream));
+  uint32_t* my_starts = reinterpret_cast<uint32_t*>(my_slot);
+  launch_bucket_starts(goff.ptr, 1, nb(), static_cast<uint32_t>(occ), my_starts, stream);
+  // ids of the remote prefix (the local bucket is last; its count is on the device)
+  launch_remote_ids_upto(d_rows, order.ptr, occ, my_starts + (U + W), d_local, send_ids.ptr, stream);
+  my_export = export_pointer(d_out);
+  TSD_CUDA(cudaMemcpyAsync(my_slot + starts_bytes, &my_export, sizeof(IpcExport), cudaMemcpyHostToDevice,
+                           stream));
+  phase_end(t);
+
+  // ---- one all-gather: every rank's bucket starts + output export --------
+  // (also the rendezvous after which peers may read our request lists)
+  TSD_CUDA(cudaEventRecord(ev_ids, stream));
+  TSD_CUDA(cudaStreamWaitEvent(comm, ev_ids, 0));
+  TSD_NCCL(ncclAllGather(my_slot, xfer.ptr, P, ncclUint8, world, comm));
+  h_xfer.resize(P * U);
+  TSD_CUDA(cudaMemcpyAsync(h_xfer.data(), xfer.ptr, P * U, cudaMemcpyDeviceToHost, comm));
+  TSD_CUDA(cudaStreamSynchronize(comm));
+  h_counts.resize(static_cast<size_t>(U) * (nb() + 1));
+  std::vector<float*> peer_out(U, nullptr);
+  for (uint32_t p = 0; p < U; ++p) {
+    std::memcpy(h_counts.data() + size_t{p} * (nb() + 1), h_xfer.data() + P * p, (nb() + 1) * 4);
+    if (p == g) continue;
+    IpcExport e;
+    std::memcpy(&e, h_xfer.data() + P * p + starts_bytes, sizeof(e));
+    peer_out[p] = static_cast<float*>(peers.open(static_cast<int>(p), e));
+  }
+  ExchangePlan xp;
+  exchange_plan(N, W, g, h_counts.data(), &xp);
+  send_off = xp.send_off;
+  send_cnt = xp.send_cnt;
+  recv_off = xp.recv_off;
+  recv_cnt = xp.recv_cnt;
+  recv_before = xp.recv_before;
+  recv_total = xp.recv_total;
+  n_remote = xp.n_remote;
+  n_local_occ = occ - n_remote;
+  recv_ids.ensure(recv_total);
+  recv_pos.ensure(recv_total);
+
+  // ---- comm stream: pull request lists, serve rows into peers' outputs ----
+  PullTable pt{};
+  ServeTable st{};
+  const auto start_of = [&](uint32_t p, uint32_t b) -> uint64_t { return h_counts[size_t{p} * (nb() + 1) + b]; };
+  for (uint32_t p = 0; p < U; ++p) {
+    if (p == g) continue;
+    if (recv_cnt[2 * p]) {
+      pt.seg[pt.nseg++] = PullSeg{peer_ids[p], peer_pos[p], start_of(p, g), recv_off[2 * p], recv_cnt[2 * p]};
+    }
+    if (recv_cnt[2 * p + 1]) {
+      pt.seg[pt.nseg++] = PullSeg{peer_ids[p], peer_pos[p], start_of(p, U + slot), recv_off[2 * p + 1],
+                                  recv_cnt[2 * p + 1]};
+    }
+    ServeTarget& tg = st.t[st.n++];
+    tg.out = peer_out[p];
+    tg.loss_slots = peer_loss[p] + static_cast<uint64_t>(g) * kServeGrid;
+    tg.r_begin = recv_off[2 * p];
+    tg.r_end = recv_off[2 * p] + recv_cnt[2 * p] + recv_cnt[2 * p + 1];
+  }
+  pt.total = recv_total;
+  t = phase_begin(kPhaseExchangeFwd, comm);
+  launch_pull_requests(pt, recv_ids.ptr, recv_pos.ptr, comm);
+  launch_serve_rows(d_w, recv_ids.ptr, recv_pos.ptr, st, cfg.dim, comm);
+  barrier_on_comm();  // every server has finished storing into every output
+  phase_end(t);
+  TSD_CUDA(cudaEventRecord(ev_fwd, comm));
+
+  t = phase_begin(kPhaseGather);
+  launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, gather_grid, stream);
+  phase_end(t);
+  TSD_CUDA(cudaStreamWaitEvent(stream, ev_fwd, 0));
+  launch_loss_finalize(loss_partials.ptr, static_cast<unsigned>(gather_grid + remote_loss_slots), d_loss.ptr,
+                       stream);
+}
+
+void ts_table::backward_p2p(const float* d_grad) {
+  using namespace tsd;
+  const uint64_t occ = last_occ;
+  const RemapView rv = remap_view();
+  OptParams opt;
+  opt.optimizer = cfg.optimizer;
+  opt.lr = cfg.lr;
+  opt.eps = cfg.eps;
+  DenseRange d0, d1;
+  const uint64_t m = n_local_occ + recv_total;
+  last_entries = m;
+  entry_keys.ensure(m);
+  entry_vals.ensure(m);
+  ensure_sort_capacity(m);
+  SegmentScratch sc;
+  sc.long_list = long_list.ptr;
+  sc.long_count = long_count.ptr;
+  sc.piece_off = piece_off.ptr;
+  sc.partials = partials.ptr;
+  RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, ghist.ptr, goff.ptr,
+                  sort_status.ptr, sort_counters.ptr};
+  uint32_t* sk = nullptr;
+  uint32_t* sv = nullptr;
+
+  // ---- compute stream: entries, sort, segments (no gradient needed yet) ---
+  TSD_CUDA(cudaEventRecord(ev_bwd0, stream));  // our gradient is complete here
+  launch_build_entries(last_rows, order.ptr + n_remote, n_local_occ, rv, recv_ids.ptr, recv_before,
+                       recv_total, static_cast<uint32_t>(occ), entry_keys.ptr, entry_vals.ptr, stream);
+  if (dp_rows) {
+    d0 = DenseRange{0, static_cast<uint32_t>(dp_rows), dense_dp.ptr};
+    TSD_CUDA(cudaMemsetAsync(dense_dp.ptr, 0, sizeof(float) * dp_rows * cfg.dim, stream));
+  }
+  if (N > 1 && flex_rows) {
+    d1 = DenseRange{static_cast<uint32_t>(dp_rows), static_cast<uint32_t>(dp_rows + flex_rows),
+                    dense_flex.ptr};
+    TSD_CUDA(cudaMemsetAsync(dense_flex.ptr, 0, sizeof(float) * flex_rows * cfg.dim, stream));
+  }
+  int t = phase_begin(kPhaseSort);
+  radix_sort_pairs(entry_keys.ptr, entry_vals.ptr, m, bits_for(local_rows ? local_rows - 1 : 0), rb, &sk, &sv,
+                   stream);
+  phase_end(t);
+  t = phase_begin(kPhaseSegments);
+  segment_starts(sk, m, starts.ptr, nseg.ptr, seg_scratch.ptr, stream);
+  const uint32_t dense_hi = static_cast<uint32_t>(dp_rows + (N > 1 ? flex_rows : 0));
+  launch_segment_split(sk, starts.ptr, nseg.ptr, dense_hi, seg_split.ptr, stream);
+  phase_end(t);
+
+  // ---- comm stream: gradient-buffer exports (rendezvous: all grads ready) --
+  TSD_CUDA(cudaStreamWaitEvent(comm, ev_bwd0, 0));
+  t = phase_begin(kPhaseExchangeBwd, comm);
+  const IpcExport mine = export_pointer(d_grad);
+  const std::vector<uint8_t> all = allgather_bytes(&mine, sizeof(mine));
+  phase_end(t);
+  // Remote gradient rows: one NVLink-bandwidth-bound gather straight out of
+  // the requesters' gradient buffers into local HBM (overlaps the sort); the
+  // segment kernels then stay on local memory.
+  PullGrads pg{};
+  for (uint32_t p = 0; p < U; ++p) {
+    if (p == g) continue;
+    IpcExport e;
+    std::memcpy(&e, all.data() + sizeof(e) * p, sizeof(e));
+    pg.src_start[pg.nsrc] = static_cast<uint32_t>(recv_off[2 * p]);
+    pg.src[pg.nsrc++] = static_cast<const float*>(peers.open(static_cast<int>(p), e));
+  }
+  pg.src_start[pg.nsrc] = static_cast<uint32_t>(recv_total);
+  GradSource gs;
+  gs.local = d_grad;
+  gs.n_local = static_cast<uint32_t>(occ);
+  if (pull_grads) {
+    recv_rows.ensure(std::max<uint64_t>(recv_total, 1) * cfg.dim);
+    launch_pull_grads(pg, recv_pos.ptr, recv_total, recv_rows.ptr, cfg.dim, comm);
+    gs.remote = recv_rows.ptr;
+  } else {  // segment kernels load remote rows from peer memory directly
+    gs.recv_pos = recv_pos.ptr;
+    gs.npeer = pg.nsrc;
+    for (int k = 0; k < pg.nsrc; ++k) {
+      gs.peer[k] = pg.src[k];
+      gs.src_start[k] = pg.src_start[k];
+    }
+    gs.src_start[pg.nsrc] = pg.src_start[pg.nsrc];
+  }
+  TSD_CUDA(cudaEventRecord(ev_grads, comm));
+  TSD_CUDA(cudaStreamWaitEvent(stream, ev_grads, 0));
+
+  // ---- replicated rows first; their all-reduce overlaps the RW updates ----
+  t = phase_begin(kPhaseSegmentUpdate);
+  launch_segment_update(sk, sv, starts.ptr, seg_split.ptr, seg_split.ptr + 1, m, cfg.dim, gs, d_w, d_state,
+                        opt, d0, d1, sc, stream);
+  phase_end(t);
+  // ---- replicated tiers over peer memory: after a rendezvous (all ranks'
+  // partials written), each rank reduces its slice of the replicated rows in
+  // group-rank order, updates it and broadcasts it to every replica --------
+  TSD_CUDA(cudaEventRecord(ev_dense, stream));
+  TSD_CUDA(cudaStreamWaitEvent(comm, ev_dense, 0));
+  cudaStream_t rs = replica_concurrent ? comm : stream;
+  t = phase_begin(kPhaseReplicaUpdate, comm);
+  barrier_on_comm();
+  if (!replica_concurrent) {
+    phase_end(t);
+    TSD_CUDA(cudaEventRecord(ev_ar, comm));
+    TSD_CUDA(cudaStreamWaitEvent(stream, ev_ar, 0));
+    t = phase_begin(kPhaseReplicaUpdate, stream);
+  }
+  if (dp_rows) {
+    ReplicaGroup grp;
+    grp.size = static_cast<int>(U);
+    grp.me = static_cast<int>(g);
+    grp.rows = static_cast<uint32_t>(dp_rows);
+    grp.row_lo = 0;
+    for (uint32_t p = 0; p < U; ++p) {
+      grp.grads[p] = peer_dense_dp[p];
+      grp.weights[p] = peer_w[p];
+      grp.state[p] = peer_state[p];
+    }
+    launch_replica_update(grp, cfg.dim, opt, rs);
+  }
+  if (N > 1 && flex_rows) {
+    ReplicaGroup grp;  // same slot in every node, node order
+    grp.size = static_cast<int>(N);
+    grp.me = static_cast<int>(node);
+    grp.rows = static_cast<uint32_t>(flex_rows);
+    grp.row_lo = static_cast<uint32_t>(dp_rows);
+    for (uint32_t k = 0; k < N; ++k) {
+      const uint32_t p = k * W + slot;
+      grp.grads[k] = peer_dense_flex[p];
+      grp.weights[k] = peer_w[p] + dp_rows * cfg.dim;
+      grp.state[k] = peer_state[p] ? peer_state[p] + dp_rows : nullptr;
+    }
+    launch_replica_update(grp, cfg.dim, opt, rs);
+  }
+  phase_end(t);
+  if (replica_concurrent) TSD_CUDA(cudaEventRecord(ev_ar, comm));
+  t = phase_begin(kPhaseSegmentUpdate);
+  launch_segment_update(sk, sv, starts.ptr, seg_split.ptr + 1, nseg.ptr, m, cfg.dim, gs, d_w, d_state, opt,
+                        d0, d1, sc, stream);
+  phase_end(t);
+  if (replica_concurrent) TSD_CUDA(cudaStreamWaitEvent(stream, ev_ar, 0));
+  // peers store into our replicated rows: the next step's rendezvous (its
+  // all-gather on the comm stream, after this stream's work) orders those
+  // stores before any of our reads
+  TSD_CUDA(cudaEventRecord(ev_ar, stream));
+  TSD_CUDA(cudaStreamWaitEvent(comm, ev_ar, 0));
 }
 
 void ts_table::destroy() {
@@ -843,6 +1250,23 @@ ts_status ts_table_phase_times(ts_table* t, double* ms, uint64_t* launches, int 
       if (launches) launches[i] = t->phase_launches[i];
     }
     if (count) *count = tsd::kNumPhases;
+  });
+}
+
+ts_status ts_table_phase_trace(ts_table* t, int* phase, int* stream_id, double* t0_ms, double* t1_ms,
+                               int capacity, int* count) {
+  return tsd::guarded([&] {
+    if (!t) tsd::fail(TS_ERR_CONFIG, "ts_table_phase_trace: null table");
+    TSD_CUDA(cudaSetDevice(t->cfg.device));
+    t->collect_timing();
+    const int n = std::min<int>(capacity, static_cast<int>(t->trace.size()));
+    for (int i = 0; i < n; ++i) {
+      if (phase) phase[i] = t->trace[i].phase;
+      if (stream_id) stream_id[i] = t->trace[i].stream_id;
+      if (t0_ms) t0_ms[i] = t->trace[i].t0;
+      if (t1_ms) t1_ms[i] = t->trace[i].t1;
+    }
+    if (count) *count = static_cast<int>(t->trace.size());
   });
 }
 

@@ -43,8 +43,14 @@ def free_port():
     return p
 
 
-@pytest.mark.parametrize("n_nodes,w,opt", [(1, 2, 1), (2, 1, 1), (2, 1, 0), (2, 2, 1), (1, 4, 1)])
-def test_nccl_path_matches_oracle(cuda, tmp_path, n_nodes, w, opt):
+CASES = [(1, 2, 1, "p2p"), (2, 1, 1, "p2p"), (2, 1, 0, "p2p"), (2, 2, 1, "p2p"), (1, 4, 1, "p2p"),
+         (1, 2, 1, "nccl"), (2, 2, 1, "nccl"), (2, 1, 0, "nccl")]
+
+
+@pytest.mark.parametrize("n_nodes,w,opt,exchange", CASES)
+def test_multi_gpu_matches_oracle(cuda, tmp_path, n_nodes, w, opt, exchange):
+    """exchange: "p2p" = fused peer-memory gather/reads (default on one node),
+    "nccl" = staged NCCL all-to-allv (TIERSHARD_EXCHANGE=nccl)."""
     u = n_nodes * w
     if n_devices() < u:
         pytest.skip(f"needs {u} GPUs")
@@ -52,7 +58,8 @@ def test_nccl_path_matches_oracle(cuda, tmp_path, n_nodes, w, opt):
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
            str(ROOT / "tests" / "mg_worker.py"), "--nodes", str(n_nodes), "--gpus-per-node", str(w),
            "--optimizer", str(opt), "--lr", str(LR), "--out", str(tmp_path)]
-    proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    env = dict(os.environ, TIERSHARD_EXCHANGE=exchange)
+    proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
     pb = mg_worker.problem(n_nodes, w)
     res = [np.load(tmp_path / f"rank{g}.npz") for g in range(u)]
