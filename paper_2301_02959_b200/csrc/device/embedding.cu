@@ -618,18 +618,42 @@ __global__ void segment_split_kernel(const uint32_t* __restrict__ keys,
                                      const uint32_t* __restrict__ starts,
                                      const uint32_t* __restrict__ d_nseg, uint32_t split_key,
                                      uint32_t* __restrict__ out) {
-  uint32_t lo = 0, hi = *d_nseg;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (keys[starts[mid]] < split_key) lo = mid + 1; else hi = mid;
+  // One warp, 33-ary search: each round probes 32 evenly spaced segments in
+  // parallel, so a 2^21-segment range resolves in ~4 dependent round trips.
+  const unsigned lane = threadIdx.x & 31u;
+  uint32_t lo = 0, hi = *d_nseg;  // answer in [lo, hi]
+  while (hi > lo) {
+    const uint32_t span = hi - lo;
+    const uint32_t probe = lo + static_cast<uint32_t>((static_cast<uint64_t>(span) * (lane + 1)) / 33);
+    const bool below = probe < hi && keys[starts[probe]] < split_key;
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, below);
+    // probes are increasing: `below` holds for a prefix of lanes
+    const int nb = __popc(b);
+    const uint32_t new_lo = nb == 0 ? lo : lo + static_cast<uint32_t>((static_cast<uint64_t>(span) * nb) / 33) + 1;
+    const uint32_t new_hi = nb == 32 ? hi : lo + static_cast<uint32_t>((static_cast<uint64_t>(span) * (nb + 1)) / 33);
+    if (span <= 32) {  // finish linearly
+      uint32_t ans = hi;
+      for (uint32_t j = lo; j < hi; ++j) {
+        if (!(keys[starts[j]] < split_key)) {
+          ans = j;
+          break;
+        }
+      }
+      lo = hi = ans;
+      break;
+    }
+    lo = new_lo;
+    hi = new_hi;
   }
-  out[0] = 0;
-  out[1] = lo;
+  if (lane == 0) {
+    out[0] = 0;
+    out[1] = lo;
+  }
 }
 
 void launch_segment_split(const uint32_t* keys, const uint32_t* starts, const uint32_t* d_nseg,
                           uint32_t split_key, uint32_t* out, cudaStream_t stream) {
-  segment_split_kernel<<<1, 1, 0, stream>>>(keys, starts, d_nseg, split_key, out);
+  segment_split_kernel<<<1, 32, 0, stream>>>(keys, starts, d_nseg, split_key, out);
   TSD_LAUNCH_CHECK();
 }
 

@@ -284,46 +284,71 @@ onesweep_pass_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __res
 // segment starts
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ bool is_head(const uint32_t* keys, uint64_t i) {
-  return i == 0 || keys[i] != keys[i - 1];
+// Head flags of one warp sub-tile (512 consecutive items, 16 coalesced rounds
+// of 32): bit `lane` of mask[r] is set when item base + 32r + lane starts a run.
+__device__ __forceinline__ void head_masks(const uint32_t* __restrict__ keys, uint64_t n, uint64_t base,
+                                           unsigned (&mask)[kScanItems]) {
+  const unsigned lane = threadIdx.x & 31u;
+  uint32_t key[kScanItems];
+#pragma unroll
+  for (int r = 0; r < kScanItems; ++r) {
+    const uint64_t i = base + static_cast<uint64_t>(r) * 32 + lane;
+    key[r] = i < n ? __ldg(keys + i) : 0u;
+  }
+  const uint32_t before = (base > 0 && base - 1 < n) ? __ldg(keys + base - 1) : ~key[0];
+#pragma unroll
+  for (int r = 0; r < kScanItems; ++r) {
+    const uint64_t i = base + static_cast<uint64_t>(r) * 32 + lane;
+    uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, key[r], 1);
+    const uint32_t last_prev_round = __shfl_sync(0xFFFFFFFFu, r == 0 ? before : key[r > 0 ? r - 1 : 0], 31);
+    if (lane == 0) prev = r == 0 ? before : last_prev_round;
+    const bool head = i < n && (i == 0 || key[r] != prev);
+    mask[r] = __ballot_sync(0xFFFFFFFFu, head);
+  }
 }
 
 __global__ void __launch_bounds__(kScanThreads)
 heads_count_kernel(const uint32_t* __restrict__ keys, uint64_t n, uint32_t* __restrict__ tile_cnt) {
-  __shared__ uint32_t s_warp[kScanThreads / 32 + 1];
-  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile;
+  __shared__ uint32_t s_cnt[kScanThreads / 32];
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile + static_cast<uint64_t>(warp) * 32 * kScanItems;
+  unsigned mask[kScanItems];
+  head_masks(keys, n, base, mask);
   uint32_t c = 0;
-#pragma unroll 4
-  for (int k = 0; k < kScanItems; ++k) {
-    const uint64_t i = base + static_cast<uint64_t>(k) * kScanThreads + threadIdx.x;
-    if (i < n && is_head(keys, i)) ++c;
+#pragma unroll
+  for (int r = 0; r < kScanItems; ++r) c += __popc(mask[r]);
+  if (lane == 0) s_cnt[warp] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t total = 0;
+    for (int w = 0; w < kScanThreads / 32; ++w) total += s_cnt[w];
+    tile_cnt[blockIdx.x] = total;
   }
-  uint32_t total;
-  block_exclusive_scan<kScanThreads>(c, s_warp, &total);
-  if (threadIdx.x == 0) tile_cnt[blockIdx.x] = total;
 }
 
 __global__ void __launch_bounds__(kScanThreads)
 heads_write_kernel(const uint32_t* __restrict__ keys, uint64_t n,
                    const uint32_t* __restrict__ tile_off, uint32_t* __restrict__ starts,
                    const uint32_t* __restrict__ d_nseg) {
-  __shared__ uint32_t s_warp[kScanThreads / 32 + 1];
-  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile +
-                        static_cast<uint64_t>(threadIdx.x) * kScanItems;
-  uint32_t flags = 0, c = 0;
+  __shared__ uint32_t s_cnt[kScanThreads / 32];
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile + static_cast<uint64_t>(warp) * 32 * kScanItems;
+  unsigned mask[kScanItems];
+  head_masks(keys, n, base, mask);
+  uint32_t c = 0;
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    const uint64_t i = base + k;
-    if (i < n && is_head(keys, i)) {
-      flags |= 1u << k;
-      ++c;
+  for (int r = 0; r < kScanItems; ++r) c += __popc(mask[r]);
+  if (lane == 0) s_cnt[warp] = c;
+  __syncthreads();
+  uint32_t pos = tile_off[blockIdx.x];
+  for (unsigned w = 0; w < warp; ++w) pos += s_cnt[w];  // sub-tiles in warp order
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int r = 0; r < kScanItems; ++r) {
+    if (mask[r] & (1u << lane)) {
+      starts[pos + __popc(mask[r] & lt)] = static_cast<uint32_t>(base + static_cast<uint64_t>(r) * 32 + lane);
     }
-  }
-  uint32_t total;
-  uint32_t pos = block_exclusive_scan<kScanThreads>(c, s_warp, &total) + tile_off[blockIdx.x];
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    if (flags & (1u << k)) starts[pos++] = static_cast<uint32_t>(base + k);
+    pos += __popc(mask[r]);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) starts[*d_nseg] = static_cast<uint32_t>(n);
 }

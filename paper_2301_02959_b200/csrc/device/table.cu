@@ -661,7 +661,7 @@ void ts_table::backward(const float* d_grad) {
     phase_end(t);
     t = phase_begin(kPhaseSegments);
     segment_starts(sk, occ, starts.ptr, nseg.ptr, seg_scratch.ptr, stream);
-    launch_segment_split(sk, starts.ptr, nseg.ptr, 0u, seg_split.ptr, stream);  // [0] = 0
+    TSD_CUDA(cudaMemsetAsync(seg_split.ptr, 0, sizeof(uint32_t), stream));  // range [0, nseg)
     phase_end(t);
     t = phase_begin(kPhaseSegmentUpdate);
     launch_segment_update(sk, sv, starts.ptr, seg_split.ptr, nseg.ptr, occ, cfg.dim, gs, d_w, d_state,
