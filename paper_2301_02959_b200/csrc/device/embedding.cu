@@ -8,6 +8,9 @@
 // oracle/restate.c replays, so single-GPU results are bit-identical.
 // Every floating-point op in the update is an explicit _rn intrinsic: no
 // contraction or fast-math can change a bit.
+#include <cstdlib>
+#include <string>
+
 #include "common.cuh"
 #include "embedding.cuh"
 #include "primitives.cuh"
@@ -340,6 +343,162 @@ __device__ __forceinline__ void group_finish_row(uint32_t row, const float (&g)[
   store_vec<PER>(wp, w);
 }
 
+// ---------------------------------------------------------------------------
+// Short segments, two interleaved per lane group.  A group of G lanes owns
+// segment pairs (j, j + ngroups); both pairs' metadata, first two gradient
+// rows, weight rows and Adagrad state are issued before any is consumed, so a
+// pair costs ~3 dependent memory round trips instead of ~4 per segment.  Per
+// segment the fp32 summation order is unchanged (entries left to right).
+// ---------------------------------------------------------------------------
+
+template <int DIM, int G>
+struct Grp {
+  static constexpr int PER = DIM / G;  // floats per lane
+  static constexpr int K = 32 / G;     // oracle virtual lanes per lane
+  static constexpr int V = DIM / 32;   // floats per virtual lane
+};
+
+// Optimizer step on one row whose weights / state are already in registers.
+template <int DIM, int G>
+__device__ __forceinline__ void group_apply(uint32_t row, const float (&g)[Grp<DIM, G>::PER],
+                                            float (&w)[Grp<DIM, G>::PER], float st, unsigned gl,
+                                            unsigned gmask, float* __restrict__ weights,
+                                            float* __restrict__ state, const OptParams& opt) {
+  constexpr int PER = Grp<DIM, G>::PER, K = Grp<DIM, G>::K, V = Grp<DIM, G>::V;
+  if (opt.optimizer == TS_OPT_SGD) {
+#pragma unroll
+    for (int j = 0; j < PER; ++j) w[j] = __fmaf_rn(-opt.lr, g[j], w[j]);
+  } else {
+    float q[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc = __fmaf_rn(g[k * V + j], g[k * V + j], acc);
+      q[k] = acc;
+    }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      if (m >= K) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) q[k] = __fadd_rn(q[k], __shfl_xor_sync(gmask, q[k], m / K));
+      } else {
+        float nq[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) nq[k] = __fadd_rn(q[k], q[k ^ m]);
+#pragma unroll
+        for (int k = 0; k < K; ++k) q[k] = nq[k];
+      }
+    }
+    const float Gs = __fadd_rn(st, __fdiv_rn(q[0], static_cast<float>(DIM)));
+    if (gl == 0) state[row] = Gs;
+    const float denom = __fadd_rn(__fsqrt_rn(Gs), opt.eps);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) w[j] = __fmaf_rn(-opt.lr, __fdiv_rn(g[j], denom), w[j]);
+  }
+  store_vec<PER>(weights + static_cast<uint64_t>(row) * DIM + static_cast<uint64_t>(gl) * PER, w);
+}
+
+__device__ __forceinline__ bool in_dense(uint32_t row, const DenseRange& d0, const DenseRange& d1) {
+  return (row >= d0.lo && row < d0.hi) || (row >= d1.lo && row < d1.hi);
+}
+
+template <int DIM, int G>
+__device__ __forceinline__ void dense_store(uint32_t row, const float (&g)[Grp<DIM, G>::PER], unsigned gl,
+                                            const DenseRange& d0, const DenseRange& d1) {
+  constexpr int PER = Grp<DIM, G>::PER;
+  const DenseRange& d = (row >= d0.lo && row < d0.hi) ? d0 : d1;
+  store_vec<PER>(d.grad + static_cast<uint64_t>(row - d.lo) * DIM + static_cast<uint64_t>(gl) * PER, g);
+}
+
+// acc += rows vals[k..e) (left to right), two rows in flight.
+template <int DIM, int G>
+__device__ __forceinline__ void sum_tail(const uint32_t* __restrict__ vals, uint32_t k, uint32_t e,
+                                         const GradSource& gs, uint64_t col,
+                                         float (&acc)[Grp<DIM, G>::PER]) {
+  constexpr int PER = Grp<DIM, G>::PER;
+  for (; k + 2 <= e; k += 2) {
+    float r0[PER], r1[PER];
+    load_vec<PER>(grad_row<1>(gs, __ldg(vals + k), DIM) + col, r0);
+    load_vec<PER>(grad_row<1>(gs, __ldg(vals + k + 1), DIM) + col, r1);
+#pragma unroll
+    for (int q = 0; q < PER; ++q) acc[q] = __fadd_rn(__fadd_rn(acc[q], r0[q]), r1[q]);
+  }
+  if (k < e) {
+    float r0[PER];
+    load_vec<PER>(grad_row<1>(gs, __ldg(vals + k), DIM) + col, r0);
+#pragma unroll
+    for (int q = 0; q < PER; ++q) acc[q] = __fadd_rn(acc[q], r0[q]);
+  }
+}
+
+template <int DIM, int G>
+__global__ void __launch_bounds__(kThreads)
+seg_pair_kernel(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ starts,
+                const uint32_t* __restrict__ seg_keys, const uint32_t* __restrict__ d_lo,
+                const uint32_t* __restrict__ d_hi, GradSource gs, float* __restrict__ weights,
+                float* __restrict__ state, OptParams opt, DenseRange d0, DenseRange d1,
+                uint32_t* __restrict__ long_list, uint32_t* __restrict__ long_count) {
+  constexpr int PER = Grp<DIM, G>::PER;
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned group = lane / G, gl = lane % G;
+  const unsigned gmask = G == 32 ? 0xFFFFFFFFu : (((1u << G) - 1u) << (group * G));
+  const uint32_t seg_lo = *d_lo, seg_hi = *d_hi;
+  const uint32_t gid = ((blockIdx.x * kThreads + threadIdx.x) >> 5) * (32 / G) + group;
+  const uint32_t ngroups = ((gridDim.x * kThreads) >> 5) * (32 / G);
+  const uint64_t col = static_cast<uint64_t>(gl) * PER;
+  const bool adagrad = opt.optimizer != TS_OPT_SGD;
+  for (uint32_t ja = seg_lo + gid; ja < seg_hi; ja += 2 * ngroups) {
+    const uint32_t jb = ja + ngroups;
+    const bool has_b = jb < seg_hi;
+    // round 1: segment metadata of both
+    const uint32_t sa = __ldg(starts + ja), ea = __ldg(starts + ja + 1), ka = __ldg(seg_keys + ja);
+    const uint32_t sb = has_b ? __ldg(starts + jb) : 0u, eb = has_b ? __ldg(starts + jb + 1) : 0u;
+    const uint32_t kb = has_b ? __ldg(seg_keys + jb) : 0u;
+    const bool long_a = ea - sa > kPiece, long_b = has_b && eb - sb > kPiece;
+    if (gl == 0) {
+      if (long_a) long_list[atomicAdd(long_count, 1u)] = ja;
+      if (long_b) long_list[atomicAdd(long_count, 1u)] = jb;
+    }
+    const bool do_a = !long_a, do_b = has_b && !long_b;
+    const bool upd_a = do_a && !in_dense(ka, d0, d1), upd_b = do_b && !in_dense(kb, d0, d1);
+    // round 2: first two entries' gradient rows, weight rows, state
+    float acc_a[PER], acc_b[PER], r_a[PER], r_b[PER], w_a[PER], w_b[PER];
+    float st_a = 0.0f, st_b = 0.0f;
+    const bool two_a = do_a && ea - sa >= 2, two_b = do_b && eb - sb >= 2;
+    if (do_a) load_vec<PER>(grad_row<1>(gs, __ldg(vals + sa), DIM) + col, acc_a);
+    if (do_b) load_vec<PER>(grad_row<1>(gs, __ldg(vals + sb), DIM) + col, acc_b);
+    if (two_a) load_vec<PER>(grad_row<1>(gs, __ldg(vals + sa + 1), DIM) + col, r_a);
+    if (two_b) load_vec<PER>(grad_row<1>(gs, __ldg(vals + sb + 1), DIM) + col, r_b);
+    if (upd_a) {
+      load_vec<PER>(weights + static_cast<uint64_t>(ka) * DIM + col, w_a);
+      if (adagrad) st_a = state[ka];
+    }
+    if (upd_b) {
+      load_vec<PER>(weights + static_cast<uint64_t>(kb) * DIM + col, w_b);
+      if (adagrad) st_b = state[kb];
+    }
+    if (two_a) {
+#pragma unroll
+      for (int q = 0; q < PER; ++q) acc_a[q] = __fadd_rn(acc_a[q], r_a[q]);
+      sum_tail<DIM, G>(vals, sa + 2, ea, gs, col, acc_a);
+    }
+    if (two_b) {
+#pragma unroll
+      for (int q = 0; q < PER; ++q) acc_b[q] = __fadd_rn(acc_b[q], r_b[q]);
+      sum_tail<DIM, G>(vals, sb + 2, eb, gs, col, acc_b);
+    }
+    if (do_a) {
+      if (upd_a) group_apply<DIM, G>(ka, acc_a, w_a, st_a, gl, gmask, weights, state, opt);
+      else dense_store<DIM, G>(ka, acc_a, gl, d0, d1);
+    }
+    if (do_b) {
+      if (upd_b) group_apply<DIM, G>(kb, acc_b, w_b, st_b, gl, gmask, weights, state, opt);
+      else dense_store<DIM, G>(kb, acc_b, gl, d0, d1);
+    }
+  }
+}
+
 template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 seg_short_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
@@ -657,10 +816,30 @@ void launch_segment_split(const uint32_t* keys, const uint32_t* starts, const ui
   TSD_LAUNCH_CHECK();
 }
 
+// Short-segment kernel choice: TIERSHARD_SEG=single (default) | pair.
+// Measured on B200 at C2 (N=1, segment_update phase): single 0.756 ms,
+// pair G=16 0.861 ms, pair G=8 1.177 ms — the pair kernel's extra ILP costs
+// more in occupancy (80 / 152 registers) than it buys; kept as an option.
+// TIERSHARD_SEG_G = lanes per segment for the pair kernel at dim 128.
+int seg_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("TIERSHARD_SEG");
+    return e && std::string(e) == "pair" ? 1 : 0;
+  }();
+  return v;
+}
+int seg_group_128() {
+  static const int v = [] {
+    const char* e = std::getenv("TIERSHARD_SEG_G");
+    return e && std::string(e) == "8" ? 8 : 16;
+  }();
+  return v;
+}
+
 void launch_segment_update(const uint32_t* keys, const uint32_t* vals, const uint32_t* starts,
-                           const uint32_t* d_lo, const uint32_t* d_hi, uint64_t n_entries,
-                           uint32_t dim, const GradSource& grads, float* weights, float* state,
-                           const OptParams& opt, const DenseRange& dense0,
+                           const uint32_t* seg_keys, const uint32_t* d_lo, const uint32_t* d_hi,
+                           uint64_t n_entries, uint32_t dim, const GradSource& grads, float* weights,
+                           float* state, const OptParams& opt, const DenseRange& dense0,
                            const DenseRange& dense1, const SegmentScratch& sc,
                            cudaStream_t stream) {
   if (n_entries == 0) return;
@@ -668,9 +847,22 @@ void launch_segment_update(const uint32_t* keys, const uint32_t* vals, const uin
   const unsigned grid = persistent_grid(g_compute_blocks_per_sm);
   dispatch_dim(dim, [&](auto D) {
     constexpr int DIM = decltype(D)::value;
-    seg_short_kernel<DIM><<<grid, kThreads, 0, stream>>>(keys, vals, starts, d_lo, d_hi, grads,
-                                                         weights, state, opt, dense0, dense1,
-                                                         sc.long_list, sc.long_count);
+    if (seg_variant() == 0 || DIM > 128) {
+      seg_short_kernel<DIM><<<grid, kThreads, 0, stream>>>(keys, vals, starts, d_lo, d_hi, grads,
+                                                           weights, state, opt, dense0, dense1,
+                                                           sc.long_list, sc.long_count);
+    } else if (DIM == 128 && seg_group_128() == 16) {
+      if constexpr (DIM == 128) {
+        seg_pair_kernel<DIM, 16><<<grid, kThreads, 0, stream>>>(vals, starts, seg_keys, d_lo, d_hi, grads,
+                                                               weights, state, opt, dense0, dense1,
+                                                               sc.long_list, sc.long_count);
+      }
+    } else {
+      constexpr int G = 8;  // DIM <= 128 here
+      if constexpr (DIM <= 128) seg_pair_kernel<DIM, G><<<grid, kThreads, 0, stream>>>(vals, starts, seg_keys, d_lo, d_hi, grads,
+                                                            weights, state, opt, dense0, dense1,
+                                                            sc.long_list, sc.long_count);
+    }
     TSD_LAUNCH_CHECK();
     long_prefix_kernel<<<1, 1024, 0, stream>>>(sc.long_list, sc.long_count, starts, sc.piece_off);
     TSD_LAUNCH_CHECK();

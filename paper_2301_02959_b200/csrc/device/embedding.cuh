@@ -85,9 +85,9 @@ struct SegmentScratch {
 // Segments [*d_lo, *d_hi) (device scalars, so ranges can be chosen on the
 // device without a host sync).
 void launch_segment_update(const uint32_t* keys, const uint32_t* vals, const uint32_t* starts,
-                           const uint32_t* d_lo, const uint32_t* d_hi, uint64_t n_entries,
-                           uint32_t dim, const GradSource& grads, float* weights, float* state,
-                           const OptParams& opt, const DenseRange& dense0,
+                           const uint32_t* seg_keys, const uint32_t* d_lo, const uint32_t* d_hi,
+                           uint64_t n_entries, uint32_t dim, const GradSource& grads, float* weights,
+                           float* state, const OptParams& opt, const DenseRange& dense0,
                            const DenseRange& dense1, const SegmentScratch& scratch,
                            cudaStream_t stream);
 

@@ -287,9 +287,8 @@ onesweep_pass_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __res
 // Head flags of one warp sub-tile (512 consecutive items, 16 coalesced rounds
 // of 32): bit `lane` of mask[r] is set when item base + 32r + lane starts a run.
 __device__ __forceinline__ void head_masks(const uint32_t* __restrict__ keys, uint64_t n, uint64_t base,
-                                           unsigned (&mask)[kScanItems]) {
+                                           unsigned (&mask)[kScanItems], uint32_t (&key)[kScanItems]) {
   const unsigned lane = threadIdx.x & 31u;
-  uint32_t key[kScanItems];
 #pragma unroll
   for (int r = 0; r < kScanItems; ++r) {
     const uint64_t i = base + static_cast<uint64_t>(r) * 32 + lane;
@@ -313,7 +312,8 @@ heads_count_kernel(const uint32_t* __restrict__ keys, uint64_t n, uint32_t* __re
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile + static_cast<uint64_t>(warp) * 32 * kScanItems;
   unsigned mask[kScanItems];
-  head_masks(keys, n, base, mask);
+  uint32_t key[kScanItems];
+  head_masks(keys, n, base, mask, key);
   uint32_t c = 0;
 #pragma unroll
   for (int r = 0; r < kScanItems; ++r) c += __popc(mask[r]);
@@ -329,12 +329,13 @@ heads_count_kernel(const uint32_t* __restrict__ keys, uint64_t n, uint32_t* __re
 __global__ void __launch_bounds__(kScanThreads)
 heads_write_kernel(const uint32_t* __restrict__ keys, uint64_t n,
                    const uint32_t* __restrict__ tile_off, uint32_t* __restrict__ starts,
-                   const uint32_t* __restrict__ d_nseg) {
+                   uint32_t* __restrict__ seg_keys, const uint32_t* __restrict__ d_nseg) {
   __shared__ uint32_t s_cnt[kScanThreads / 32];
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile + static_cast<uint64_t>(warp) * 32 * kScanItems;
   unsigned mask[kScanItems];
-  head_masks(keys, n, base, mask);
+  uint32_t key[kScanItems];
+  head_masks(keys, n, base, mask, key);
   uint32_t c = 0;
 #pragma unroll
   for (int r = 0; r < kScanItems; ++r) c += __popc(mask[r]);
@@ -346,7 +347,9 @@ heads_write_kernel(const uint32_t* __restrict__ keys, uint64_t n,
 #pragma unroll
   for (int r = 0; r < kScanItems; ++r) {
     if (mask[r] & (1u << lane)) {
-      starts[pos + __popc(mask[r] & lt)] = static_cast<uint32_t>(base + static_cast<uint64_t>(r) * 32 + lane);
+      const uint32_t j = pos + __popc(mask[r] & lt);
+      starts[j] = static_cast<uint32_t>(base + static_cast<uint64_t>(r) * 32 + lane);
+      if (seg_keys) seg_keys[j] = key[r];
     }
     pos += __popc(mask[r]);
   }
@@ -407,8 +410,8 @@ void radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t
   *vals_out = const_cast<uint32_t*>(cur_v);
 }
 
-void segment_starts(const uint32_t* sorted_keys, uint64_t n, uint32_t* starts, uint32_t* d_nseg,
-                    uint32_t* tile_scratch, cudaStream_t stream) {
+void segment_starts(const uint32_t* sorted_keys, uint64_t n, uint32_t* starts, uint32_t* seg_keys,
+                    uint32_t* d_nseg, uint32_t* tile_scratch, cudaStream_t stream) {
   if (n == 0) {
     TSD_CUDA(cudaMemsetAsync(d_nseg, 0, sizeof(uint32_t), stream));
     TSD_CUDA(cudaMemsetAsync(starts, 0, sizeof(uint32_t), stream));
@@ -422,7 +425,7 @@ void segment_starts(const uint32_t* sorted_keys, uint64_t n, uint32_t* starts, u
   TSD_LAUNCH_CHECK();
   device_exclusive_scan(tile_cnt, tile_off, tiles, scratch, d_nseg, stream);
   heads_write_kernel<<<static_cast<unsigned>(tiles), kScanThreads, 0, stream>>>(sorted_keys, n, tile_off,
-                                                                                starts, d_nseg);
+                                                                                starts, seg_keys, d_nseg);
   TSD_LAUNCH_CHECK();
 }
 

@@ -71,7 +71,8 @@ void radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t
 // Segment starts of sorted keys: starts[j] = first index of the j-th run of
 // equal keys, starts[nseg] = n; *d_nseg receives nseg.  `flags_scratch`
 // holds scan_scratch_elems(n) + radix_tiles-style tile counts (2 * n/4096+2).
-void segment_starts(const uint32_t* sorted_keys, uint64_t n, uint32_t* starts,
+// seg_keys (nullable) receives the key of every segment.
+void segment_starts(const uint32_t* sorted_keys, uint64_t n, uint32_t* starts, uint32_t* seg_keys,
                     uint32_t* d_nseg, uint32_t* tile_scratch, cudaStream_t stream);
 inline uint64_t segment_scratch_elems(uint64_t n) {
   return 2 * ((n + kScanTile - 1) / kScanTile) + 4 + scan_scratch_elems((n + kScanTile - 1) / kScanTile);

@@ -125,7 +125,7 @@ struct ts_table {
   // dedup / sort
   tsd::DevBuf<uint32_t> keys_a, vals_a, keys_b, vals_b, ghist, goff, sort_counters;
   tsd::DevBuf<uint64_t> sort_status;
-  tsd::DevBuf<uint32_t> starts, seg_scratch, nseg, seg_split;
+  tsd::DevBuf<uint32_t> starts, seg_keys, seg_scratch, nseg, seg_split;
   tsd::DevBuf<uint32_t> long_list, long_count, piece_off, entry_keys, entry_vals;
   tsd::DevBuf<float> partials;
   // U > 1 routing / exchange
@@ -246,6 +246,7 @@ struct ts_table {
     sort_counters.ensure(tsd::kMaxRadixPasses);
     sort_status.ensure(tsd::kMaxRadixPasses * tiles * tsd::kRadixBins);
     starts.ensure(m + 1);
+    seg_keys.ensure(m + 1);
     seg_scratch.ensure(tsd::segment_scratch_elems(m) + 8);
     const uint64_t max_long = m / (tsd::kPiece + 1) + 1;
     long_list.ensure(max_long);
@@ -660,11 +661,11 @@ void ts_table::backward(const float* d_grad) {
     radix_sort_pairs(last_rows, nullptr, occ, key_bits, rb, &sk, &sv, stream);
     phase_end(t);
     t = phase_begin(kPhaseSegments);
-    segment_starts(sk, occ, starts.ptr, nseg.ptr, seg_scratch.ptr, stream);
+    segment_starts(sk, occ, starts.ptr, seg_keys.ptr, nseg.ptr, seg_scratch.ptr, stream);
     TSD_CUDA(cudaMemsetAsync(seg_split.ptr, 0, sizeof(uint32_t), stream));  // range [0, nseg)
     phase_end(t);
     t = phase_begin(kPhaseSegmentUpdate);
-    launch_segment_update(sk, sv, starts.ptr, seg_split.ptr, nseg.ptr, occ, cfg.dim, gs, d_w, d_state,
+    launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr, nseg.ptr, occ, cfg.dim, gs, d_w, d_state,
                           opt, d0, d1, sc, stream);
     phase_end(t);
     return;
@@ -713,7 +714,7 @@ void ts_table::backward(const float* d_grad) {
   radix_sort_pairs(entry_keys.ptr, entry_vals.ptr, m, key_bits, rb, &sk, &sv, stream);
   phase_end(t);
   t = phase_begin(kPhaseSegments);
-  segment_starts(sk, m, starts.ptr, nseg.ptr, seg_scratch.ptr, stream);
+  segment_starts(sk, m, starts.ptr, seg_keys.ptr, nseg.ptr, seg_scratch.ptr, stream);
   // dense-reduced rows are the lowest local ids: split the segments there
   const uint32_t dense_hi = static_cast<uint32_t>(dp_rows + (N > 1 ? flex_rows : 0));
   launch_segment_split(sk, starts.ptr, nseg.ptr, dense_hi, seg_split.ptr, stream);
@@ -722,7 +723,7 @@ void ts_table::backward(const float* d_grad) {
 
   // ---- replicated rows first; their all-reduce overlaps the RW updates ----
   t = phase_begin(kPhaseSegmentUpdate);
-  launch_segment_update(sk, sv, starts.ptr, seg_split.ptr, seg_split.ptr + 1, m, cfg.dim, gs, d_w,
+  launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr, seg_split.ptr + 1, m, cfg.dim, gs, d_w,
                         d_state, opt, d0, d1, sc, stream);
   phase_end(t);
   TSD_CUDA(cudaEventRecord(ev_dense, stream));
@@ -741,7 +742,7 @@ void ts_table::backward(const float* d_grad) {
   TSD_CUDA(cudaEventRecord(ev_ar, comm));
 
   t = phase_begin(kPhaseSegmentUpdate);
-  launch_segment_update(sk, sv, starts.ptr, seg_split.ptr + 1, nseg.ptr, m, cfg.dim, gs, d_w, d_state,
+  launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr + 1, nseg.ptr, m, cfg.dim, gs, d_w, d_state,
                         opt, d0, d1, sc, stream);
   phase_end(t);
   TSD_CUDA(cudaStreamWaitEvent(stream, ev_ar, 0));
@@ -900,7 +901,7 @@ void ts_table::backward_p2p(const float* d_grad) {
                    stream);
   phase_end(t);
   t = phase_begin(kPhaseSegments);
-  segment_starts(sk, m, starts.ptr, nseg.ptr, seg_scratch.ptr, stream);
+  segment_starts(sk, m, starts.ptr, seg_keys.ptr, nseg.ptr, seg_scratch.ptr, stream);
   const uint32_t dense_hi = static_cast<uint32_t>(dp_rows + (N > 1 ? flex_rows : 0));
   launch_segment_split(sk, starts.ptr, nseg.ptr, dense_hi, seg_split.ptr, stream);
   phase_end(t);
@@ -944,7 +945,7 @@ void ts_table::backward_p2p(const float* d_grad) {
 
   // ---- replicated rows first; their all-reduce overlaps the RW updates ----
   t = phase_begin(kPhaseSegmentUpdate);
-  launch_segment_update(sk, sv, starts.ptr, seg_split.ptr, seg_split.ptr + 1, m, cfg.dim, gs, d_w, d_state,
+  launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr, seg_split.ptr + 1, m, cfg.dim, gs, d_w, d_state,
                         opt, d0, d1, sc, stream);
   phase_end(t);
   // ---- replicated tiers over peer memory: after a rendezvous (all ranks'
@@ -991,7 +992,7 @@ void ts_table::backward_p2p(const float* d_grad) {
   phase_end(t);
   if (replica_concurrent) TSD_CUDA(cudaEventRecord(ev_ar, comm));
   t = phase_begin(kPhaseSegmentUpdate);
-  launch_segment_update(sk, sv, starts.ptr, seg_split.ptr + 1, nseg.ptr, m, cfg.dim, gs, d_w, d_state, opt,
+  launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr + 1, nseg.ptr, m, cfg.dim, gs, d_w, d_state, opt,
                         d0, d1, sc, stream);
   phase_end(t);
   if (replica_concurrent) TSD_CUDA(cudaStreamWaitEvent(stream, ev_ar, 0));
@@ -1019,6 +1020,7 @@ void ts_table::destroy() {
   rows_dev.release();
   sort_status.release();
   seg_split.release();
+  seg_keys.release();
   for (auto* b : {&keys_a, &vals_a, &keys_b, &vals_b, &ghist, &goff, &sort_counters, &starts,
                   &seg_scratch, &nseg, &long_list, &long_count, &piece_off, &entry_keys,
                   &entry_vals, &bucket, &order, &send_ids, &recv_ids, &bucket_start, &all_counts}) {
