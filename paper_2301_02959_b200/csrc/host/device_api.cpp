@@ -1,0 +1,98 @@
+// C++ front door over the C-ABI table handle (tiershard/device.hpp).
+#include "tiershard/device.hpp"
+
+#include <cstring>
+
+#include "capi_check.hpp"
+#include "parallel.hpp"
+#include "tiershard/error.hpp"
+#include "tiershard/simulator.hpp"
+#include "tiershard_b200.h"
+
+namespace tiershard {
+
+NcclUniqueId new_nccl_unique_id() {
+  NcclUniqueId id{};
+  detail::check(ts_nccl_unique_id(id.data()));
+  return id;
+}
+
+std::vector<uint8_t> placement_bytes(const ShardingPlan& plan, const RowDistribution& dist,
+                                     const Topology& topo, uint64_t hash_seed) {
+  if (topo.total_gpus() > 256) throw ConfigError("device path: at most 256 GPUs");
+  const std::vector<RowPlacement> pl = assign_rows(plan, dist, topo, hash_seed);
+  std::vector<uint8_t> dest(pl.size(), 0);
+  detail::parallel_for(pl.size(), [&](size_t lo, size_t hi) {
+    for (size_t i = lo; i < hi; ++i) {
+      dest[i] = static_cast<uint8_t>(pl[i].tier == Tier::kFlex ? pl[i].flex_slot : pl[i].owner_gpu);
+    }
+  });
+  return dest;
+}
+
+SequenceEmbedding::SequenceEmbedding(const ShardingPlan& plan, const RowDistribution& dist,
+                                     const Topology& topo, const CostModelConfig& cfg,
+                                     const DeviceOptions& options, uint64_t hash_seed)
+    : dim_(cfg.embedding_dim), gpus_(topo.total_gpus()) {
+  cfg.validate();
+  topo.validate();
+  if (cfg.scalar_bytes != 4) throw ConfigError("device path: fp32 tables only (scalar_bytes = 4)");
+  const std::vector<uint8_t> dest = placement_bytes(plan, dist, topo, hash_seed);
+  ts_table_config c{};
+  c.num_nodes = topo.num_nodes;
+  c.gpus_per_node = topo.gpus_per_node;
+  c.rank = options.rank;
+  c.device = options.device;
+  c.dim = cfg.embedding_dim;
+  c.n_rows = dist.rows().size();
+  c.dp_cut = plan.dp_cut;
+  c.flex_cut = plan.flex_cut;
+  c.weight_seed = options.weight_seed;
+  c.optimizer = options.optimizer == Optimizer::kSgd ? TS_OPT_SGD : TS_OPT_ROWWISE_ADAGRAD;
+  c.lr = options.learning_rate;
+  c.eps = options.epsilon;
+  c.max_occurrences = options.max_occurrences;
+  c.nccl_unique_id = options.nccl_id ? options.nccl_id->data() : nullptr;
+  detail::check(ts_table_create(&table_, &c, dest.data()));
+}
+
+SequenceEmbedding::~SequenceEmbedding() {
+  if (table_) ts_table_destroy(table_);
+}
+
+void SequenceEmbedding::forward(const uint32_t* d_rows, uint64_t occurrences, float* d_out) {
+  detail::check(ts_table_forward(table_, d_rows, occurrences, d_out));
+}
+
+void SequenceEmbedding::backward(const float* d_grad) { detail::check(ts_table_backward(table_, d_grad)); }
+
+double SequenceEmbedding::train_step_host(const std::vector<uint32_t>& rows) {
+  double loss = 0.0;
+  detail::check(ts_table_train_step_host(table_, rows.data(), rows.size(), &loss));
+  return loss;
+}
+
+std::vector<uint64_t> SequenceEmbedding::counters() const {
+  std::vector<uint64_t> c(size_t{TS_NUM_COUNTERS} * gpus_);
+  detail::check(ts_table_counters(table_, c.data()));
+  return c;
+}
+
+std::vector<float> SequenceEmbedding::read_rows(const std::vector<uint32_t>& rows,
+                                                std::vector<float>* state) const {
+  std::vector<float> w(rows.size() * dim_);
+  if (state) state->assign(rows.size(), 0.0f);
+  detail::check(ts_table_read_rows(table_, rows.data(), rows.size(), w.data(),
+                                   state ? state->data() : nullptr));
+  return w;
+}
+
+void SequenceEmbedding::synchronize() const { detail::check(ts_table_synchronize(table_)); }
+
+void* SequenceEmbedding::stream() const {
+  void* s = nullptr;
+  detail::check(ts_table_stream(table_, &s));
+  return s;
+}
+
+}  // namespace tiershard

@@ -12,6 +12,9 @@ Outputs
   mini_2x4_3tier.npz   placements, 4 iterations of batches and the per-GPU
                        counter block of each iteration (restated counters,
                        verified here against the reference's SimReport)
+  io_digests.json      (--io) sha256 of every artefact oracle/_ref/ref_artifacts
+                       writes for tests/test_io_parity.py's manifests, and
+                       the reference's error text for each malformed one
 """
 from __future__ import annotations
 
@@ -82,5 +85,31 @@ def main() -> None:
         print("wrote", name + ".npz")
 
 
+def make_io_digests() -> None:
+    import test_io_parity as io
+    assert io.REF_ARTIFACTS.exists(), "build oracle/_ref first: make -C oracle ref"
+    golden = {}
+    with tempfile.TemporaryDirectory() as td:
+        tmp = Path(td)
+        for name, case in io.CASES.items():
+            for sim in (False, True):
+                base = tmp / name / ("sim" if sim else "nosim")
+                manifest = io.write_case(base / "in", *case, sim=sim)
+                code, files = io.run_artifacts(io.REF_ARTIFACTS, manifest, base / "out")
+                assert code == 0, files.get("error.txt")
+                golden[f"{name}/{'sim' if sim else 'nosim'}"] = io.digests(files)
+        for name, case in io.ERROR_CASES.items():
+            base = tmp / "err" / name
+            manifest = io.write_case(base / "in", *case, sim=False)
+            code, files = io.run_artifacts(io.REF_ARTIFACTS, manifest, base / "out")
+            assert code == 3, (name, code)
+            golden[f"error/{name}"] = files["error.txt"].decode().replace(str(base / "in"), "<dir>")
+    (HERE / "io_digests.json").write_text(json.dumps(golden, indent=1, sort_keys=True) + "\n")
+    print("wrote io_digests.json")
+
+
 if __name__ == "__main__":
-    main()
+    if "--io" in sys.argv:
+        make_io_digests()
+    else:
+        main()

@@ -53,3 +53,28 @@ def test_config_errors_before_device():
         ts.Router(10, 5, 2, np.zeros(10, np.uint8), 1, 1)
     assert e.value.kind == "ValidationError"
     assert "plan does not cover" in e.value.message
+
+
+EXAMPLE = ROOT / "paper_2301_02959_b200" / "bin" / "ts_example"
+
+
+def test_cpp_example_fails_loudly_without_device():
+    """The C++ front door (tiershard/device.hpp) plans on the host, then
+    refuses to run the table anywhere but a GPU."""
+    if ts.device_count() > 0:
+        pytest.skip("a device is present")
+    proc = subprocess.run([str(EXAMPLE), "20000", "32", "64", "1"], capture_output=True, text=True,
+                          timeout=300)
+    assert proc.returncode == 3
+    assert "no CUDA device" in proc.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_example_trains_on_device(cuda):
+    import json
+    proc = subprocess.run([str(EXAMPLE), "100000", "64", "128", "3"], capture_output=True, text=True,
+                          timeout=300)
+    assert proc.returncode == 0, proc.stdout + proc.stderr
+    doc = json.loads(proc.stdout.strip().splitlines()[-1])
+    assert doc["occurrences"] > 0 and doc["served"] > 0
+    assert doc["last_loss"] > 0
