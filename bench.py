@@ -345,12 +345,36 @@ def run_ours(args, dist: Dist):
             table.train_step_host(pinned[k % len(pinned)])
         dist.barrier()
         t0 = time.perf_counter()
+        marks = []
         for k in range(args.steps):
             table.train_step_host(pinned[k % len(pinned)])
+            marks.append(time.perf_counter())
         e2e_s = dist.max(time.perf_counter() - t0)
+        step_wall = np.diff(np.array([t0] + marks)) * 1e3
         h2d = float(np.mean([pinned[k % len(pinned)].nbytes for k in range(args.steps)]))
         e2e = {"value": samples / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": 8}
+               "d2h_bytes_per_step": 8,
+               "step_wall_ms": [round(float(np.percentile(step_wall, q)), 3) for q in (0, 50, 100)]}
+        if os.environ.get("TS_BENCH_DIAG"):
+            # diagnostic variant: same host copies, torch-owned device buffers
+            pin_t = [torch.from_numpy(b.view(np.int32)).pin_memory() for b in batches]
+            dist.barrier()
+            t1 = time.perf_counter()
+            for k in range(args.steps):
+                b = d_rows[k % len(d_rows)]
+                with torch.cuda.stream(stream):
+                    b.copy_(pin_t[k % len(pin_t)], non_blocking=True)
+                table.train_step(b.data_ptr(), b.numel(), d_out.data_ptr())
+                table.loss()
+            e2e["diag_torch_buffers_value"] = samples / dist.max(time.perf_counter() - t1)
+            torch.cuda.synchronize()
+            del pin_t  # pinned blocks carry events on the table's stream: free before it goes
+        # one more host-buffer step with the phase timeline (diagnostics)
+        table.enable_timing(True)
+        table.train_step_host(pinned[0])
+        table.phase_times()
+        e2e["step_trace_ms"] = [(n, sid, round(a, 4), round(b, 4)) for n, sid, a, b in table.phase_trace()]
+        table.enable_timing(False)
     clk = clocks.stop()
 
     # ---- roofline of the dominant kernel -----------------------------------

@@ -188,10 +188,12 @@ __device__ __forceinline__ void finish_row(uint32_t row, const float (&g)[DIM / 
   const unsigned lane = threadIdx.x & 31u;
   if (row >= d0.lo && row < d0.hi) {
     store_lane<VEC>(d0.grad + static_cast<uint64_t>(row - d0.lo) * DIM + lane * VEC, g);
+    if (d0.stamp && lane == 0) d0.stamp[row - d0.lo] = d0.epoch;
     return;
   }
   if (row >= d1.lo && row < d1.hi) {
     store_lane<VEC>(d1.grad + static_cast<uint64_t>(row - d1.lo) * DIM + lane * VEC, g);
+    if (d1.stamp && lane == 0) d1.stamp[row - d1.lo] = d1.epoch;
     return;
   }
   float* wp = weights + static_cast<uint64_t>(row) * DIM + lane * VEC;
@@ -299,10 +301,12 @@ __device__ __forceinline__ void group_finish_row(uint32_t row, const float (&g)[
   const uint64_t col = static_cast<uint64_t>(gl) * PER;
   if (row >= d0.lo && row < d0.hi) {
     store_vec<PER>(d0.grad + static_cast<uint64_t>(row - d0.lo) * DIM + col, g);
+    if (d0.stamp && gl == 0) d0.stamp[row - d0.lo] = d0.epoch;
     return;
   }
   if (row >= d1.lo && row < d1.hi) {
     store_vec<PER>(d1.grad + static_cast<uint64_t>(row - d1.lo) * DIM + col, g);
+    if (d1.stamp && gl == 0) d1.stamp[row - d1.lo] = d1.epoch;
     return;
   }
   float* wp = weights + static_cast<uint64_t>(row) * DIM + col;
@@ -409,6 +413,7 @@ __device__ __forceinline__ void dense_store(uint32_t row, const float (&g)[Grp<D
   constexpr int PER = Grp<DIM, G>::PER;
   const DenseRange& d = (row >= d0.lo && row < d0.hi) ? d0 : d1;
   store_vec<PER>(d.grad + static_cast<uint64_t>(row - d.lo) * DIM + static_cast<uint64_t>(gl) * PER, g);
+  if (d.stamp && gl == 0) d.stamp[row - d.lo] = d.epoch;
 }
 
 // acc += rows vals[k..e) (left to right), two rows in flight.
@@ -708,6 +713,71 @@ replica_update_kernel(ReplicaGroup grp, OptParams opt) {
   __threadfence_system();
 }
 
+// Stamped variant: a warp tests 32 rows' stamps at once (one 4-byte peer
+// load per member per row), then walks the rows some member touched.
+template <int DIM>
+__global__ void __launch_bounds__(kThreads)
+replica_sparse_kernel(ReplicaGroup grp, OptParams opt) {
+  constexpr int VEC = DIM / 32;
+  const unsigned lane = threadIdx.x & 31u;
+  const uint32_t per = (grp.rows + grp.size - 1) / grp.size;
+  const uint32_t lo = per * grp.me;
+  const uint32_t hi = min(grp.rows, lo + per);
+  const uint32_t gwarp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
+  float* mine = grp.weights[grp.me];
+  float* my_state = grp.state[grp.me];
+  for (uint32_t base = lo + gwarp * 32; base < hi; base += nwarps * 32) {
+    const uint32_t r = base + lane;
+    uint32_t members = 0;
+    if (r < hi) {
+      uint32_t st[kMaxGradPeers];
+#pragma unroll
+      for (int k = 0; k < kMaxGradPeers; ++k) st[k] = k < grp.size ? grp.stamps[k][r] : 0u;
+#pragma unroll
+      for (int k = 0; k < kMaxGradPeers; ++k) members |= (k < grp.size && st[k] == grp.epoch) ? 1u << k : 0u;
+    }
+    unsigned active = __ballot_sync(0xFFFFFFFFu, members != 0);
+    while (active) {
+      const int b = __ffs(active) - 1;
+      active &= active - 1;
+      const uint32_t row = base + b;
+      const uint32_t m = __shfl_sync(0xFFFFFFFFu, members, b);
+      const uint64_t off = static_cast<uint64_t>(row) * DIM + lane * VEC;
+      float part[kMaxGradPeers][VEC];
+#pragma unroll
+      for (int k = 0; k < kMaxGradPeers; ++k) {  // touched members' loads in flight
+        if ((m >> k) & 1u) load_lane<VEC>(grp.grads[k] + off, part[k]);
+      }
+      // group-rank order over the members that touched the row (an untouched
+      // member's partial is zero: adding it changes nothing)
+      float g[VEC];
+      bool first = true;
+#pragma unroll
+      for (int k = 0; k < kMaxGradPeers; ++k) {
+        if ((m >> k) & 1u) {
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) g[j] = first ? part[k][j] : __fadd_rn(g[j], part[k][j]);
+          first = false;
+        }
+      }
+      finish_row<DIM>(row, g, mine, my_state, opt, DenseRange{}, DenseRange{});
+      __syncwarp();
+      float w[VEC];
+      load_lane<VEC>(mine + off, w);
+      const float st = my_state ? my_state[row] : 0.0f;
+#pragma unroll
+      for (int k = 0; k < kMaxGradPeers; ++k) {
+        if (k < grp.size && k != grp.me) {
+          store_lane<VEC>(grp.weights[k] + off, w);
+          if (my_state && lane == 0) grp.state[k][row] = st;
+        }
+      }
+    }
+  }
+  __threadfence_system();
+}
+
 __global__ void __launch_bounds__(kThreads)
 init_weights_kernel(float* __restrict__ weights, uint64_t local_rows, uint32_t dim, uint64_t seed,
                     const uint32_t* __restrict__ l2c) {
@@ -896,7 +966,13 @@ void launch_replica_update(const ReplicaGroup& grp, uint32_t dim, const OptParam
       1, std::min<unsigned>(persistent_grid(g_compute_blocks_per_sm), ceil_div(per, kThreads / 32)));
   dispatch_dim(dim, [&](auto D) {
     constexpr int DIM = decltype(D)::value;
-    replica_update_kernel<DIM><<<grid, kThreads, 0, stream>>>(grp, opt);
+    if (grp.stamps[0]) {
+      const unsigned sgrid = std::max<unsigned>(
+          1, std::min<unsigned>(persistent_grid(g_compute_blocks_per_sm), ceil_div(per, kThreads)));
+      replica_sparse_kernel<DIM><<<sgrid, kThreads, 0, stream>>>(grp, opt);
+    } else {
+      replica_update_kernel<DIM><<<grid, kThreads, 0, stream>>>(grp, opt);
+    }
   });
   TSD_LAUNCH_CHECK();
 }

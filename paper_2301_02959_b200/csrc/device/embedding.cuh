@@ -31,9 +31,14 @@ struct OptParams {
 
 // Rows in [dense_lo, dense_hi) are not updated in place: their reduced
 // gradient is written to dense_grad[row - dense_lo] (all-reduced later).
+// With `stamp`, the row's stamp[row - dense_lo] is set to `epoch` as well:
+// the replica update then reads only rows stamped this step, so the dense
+// buffer never needs clearing and untouched rows cost no NVLink traffic.
 struct DenseRange {
   uint32_t lo = 0, hi = 0;
   float* grad = nullptr;
+  uint32_t* stamp = nullptr;
+  uint32_t epoch = 0;
 };
 
 constexpr int kMaxGradPeers = 8;
@@ -105,11 +110,16 @@ void launch_dense_update(const float* grad, uint32_t rows, uint32_t row_lo, uint
 // partial gradients grads[0..size) IN GROUP-RANK ORDER (peer loads), applies
 // the optimizer to its replica and stores the updated row (and Adagrad state)
 // into every member's replica (peer stores).  Deterministic and identical on
-// all replicas by construction.
+// all replicas by construction.  With stamps, a member's partial counts only
+// where its stamp equals `epoch` (rows it touched this step); rows no member
+// touched have a zero gradient, which leaves SGD and row-wise Adagrad rows
+// unchanged, so they are skipped without a read.
 struct ReplicaGroup {
   int size = 0;
   int me = 0;                              // my index in the group
   const float* grads[kMaxGradPeers] = {};  // dense partials [rows x dim], by group rank
+  const uint32_t* stamps[kMaxGradPeers] = {};  // per-row epoch stamps (all or none)
+  uint32_t epoch = 0;
   float* weights[kMaxGradPeers] = {};      // replicas: weights + row_lo * dim
   float* state[kMaxGradPeers] = {};        // Adagrad state + row_lo (may be null)
   uint32_t rows = 0;                       // dense rows of the tier

@@ -169,18 +169,26 @@ IpcExport export_pointer(const void* ptr) {
 }
 
 void* PeerMappings::open(int peer, const IpcExport& e) {
+  // keyed by base address, validated by handle: an exporter that freed and
+  // re-allocated at the same address sends a different handle, and the stale
+  // mapping is replaced instead of reused
   const auto key = std::make_pair(peer, e.base_id);
   auto it = opened_.find(key);
+  if (it != opened_.end() && std::memcmp(&it->second.handle, &e.handle, sizeof(e.handle)) != 0) {
+    TSD_CUDA(cudaIpcCloseMemHandle(it->second.base));
+    opened_.erase(it);
+    it = opened_.end();
+  }
   if (it == opened_.end()) {
     void* p = nullptr;
     TSD_CUDA(cudaIpcOpenMemHandle(&p, e.handle, cudaIpcMemLazyEnablePeerAccess));
-    it = opened_.emplace(key, p).first;
+    it = opened_.emplace(key, Mapping{e.handle, p}).first;
   }
-  return static_cast<char*>(it->second) + e.offset;
+  return static_cast<char*>(it->second.base) + e.offset;
 }
 
 void PeerMappings::close_all() {
-  for (auto& kv : opened_) cudaIpcCloseMemHandle(kv.second);
+  for (auto& kv : opened_) cudaIpcCloseMemHandle(kv.second.base);
   opened_.clear();
 }
 

@@ -46,7 +46,11 @@ class PeerMappings {
   ~PeerMappings() { close_all(); }
 
  private:
-  std::map<std::pair<int, uint64_t>, void*> opened_;  // (peer, base_id) -> mapped base
+  struct Mapping {
+    cudaIpcMemHandle_t handle;
+    void* base;
+  };
+  std::map<std::pair<int, uint64_t>, Mapping> opened_;  // (peer, base_id) -> mapping
 };
 
 // Request lists a server pulls: for each source rank, a run of `count`

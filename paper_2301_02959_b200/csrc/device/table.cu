@@ -122,6 +122,7 @@ struct ts_table {
   tsd::DevBuf<double> loss_partials, d_loss;
   tsd::DevBuf<unsigned long long> tier_counts;  // RW, Flex, DP of this requester
   tsd::DevBuf<uint32_t> rows_dev;                // host-step staging
+  tsd::DevBuf<float> host_out;                   // host-step output [max_occurrences x D]
   // dedup / sort
   tsd::DevBuf<uint32_t> keys_a, vals_a, keys_b, vals_b, ghist, goff, sort_counters;
   tsd::DevBuf<uint64_t> sort_status;
@@ -131,6 +132,8 @@ struct ts_table {
   // U > 1 routing / exchange
   tsd::DevBuf<uint32_t> bucket, order, send_ids, recv_ids, bucket_start, all_counts;
   tsd::DevBuf<float> send_rows, recv_rows, dense_dp, dense_flex;
+  tsd::DevBuf<uint32_t> stamp_dp, stamp_flex;  // per dense row: last epoch written (P2P)
+  uint32_t epoch = 0;                          // backward steps (P2P)
   std::vector<uint32_t> h_counts;     // [U][NB] send counts of every rank
   std::vector<uint64_t> send_off, send_cnt, recv_off, recv_cnt;  // per peer (entries)
   uint64_t n_remote = 0, n_local_occ = 0, recv_total = 0, recv_before = 0;
@@ -148,6 +151,7 @@ struct ts_table {
   std::vector<double*> peer_loss;                   // peers' remote-loss slots (mapped)
   std::vector<const float*> peer_grad;              // peers' gradient buffers (mapped)
   std::vector<const float*> peer_dense_dp, peer_dense_flex;  // peers' dense partials (mapped)
+  std::vector<const uint32_t*> peer_stamp_dp, peer_stamp_flex;  // and their row stamps
   std::vector<float*> peer_w, peer_state;           // peers' shards (mapped)
   tsd::IpcExport my_export{};                       // staging for the step payload
   uint64_t remote_loss_slots = 0;                   // U * kServeGrid
@@ -155,9 +159,12 @@ struct ts_table {
   //   TIERSHARD_REPLICA=serial|concurrent  replica update after the DP
   //     segments on the compute stream, or on the comm stream beside the RW
   //     segments;  TIERSHARD_PULL_GRADS=1|0  stage remote gradient rows into
-  //     HBM with one NVLink gather, or load them from peer memory in-kernel
+  //     HBM with one NVLink gather, or load them from peer memory in-kernel.
+  //     Staging is the default: equal on device-resident steps, and the
+  //     in-kernel peer loads measured 8x slower on the host-buffer entry
+  //     point (ts_table_train_step_host, 4.2 ms vs 0.5 ms at U = 2)
   bool replica_concurrent = true;
-  bool pull_grads = false;
+  bool pull_grads = true;
 
   size_t step_payload_bytes() const { return ((nb() + 1) * 4 + 7) / 8 * 8 + sizeof(tsd::IpcExport); }
   std::vector<uint8_t> allgather_bytes(const void* mine, size_t bytes);
@@ -376,6 +383,13 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     all_counts.ensure(static_cast<uint64_t>(U) * (nb() + 1));
     dense_dp.ensure(std::max<uint64_t>(dp_rows, 1) * c.dim);
     if (N > 1) dense_flex.ensure(std::max<uint64_t>(flex_rows, 1) * c.dim);
+    stamp_dp.ensure(std::max<uint64_t>(dp_rows, 1));
+    TSD_CUDA(cudaMemsetAsync(stamp_dp.ptr, 0, sizeof(uint32_t) * stamp_dp.cap, stream));
+    if (N > 1) {
+      stamp_flex.ensure(std::max<uint64_t>(flex_rows, 1));
+      TSD_CUDA(cudaMemsetAsync(stamp_flex.ptr, 0, sizeof(uint32_t) * stamp_flex.cap, stream));
+    }
+    TSD_CUDA(cudaStreamSynchronize(stream));
     // communicators: world, intra (color = node), cross (color = slot)
     // the exchange / replica stream gets the highest priority: its kernels
     // are short, sit on the critical path, and would otherwise queue behind
@@ -450,17 +464,18 @@ void ts_table::setup_p2p() {
   p2p = ok != 0;
   if (!p2p) return;
   if (const char* env = std::getenv("TIERSHARD_REPLICA")) replica_concurrent = std::string(env) != "serial";
-  if (const char* env = std::getenv("TIERSHARD_PULL_GRADS")) pull_grads = std::string(env) == "1";
+  if (const char* env = std::getenv("TIERSHARD_PULL_GRADS")) pull_grads = std::string(env) != "0";
   // export the table-owned buffers peers read or write
   auto exp_or_none = [](const void* p) {
     IpcExport e;
     std::memset(&e, 0, sizeof(e));
     return p ? export_pointer(p) : e;
   };
-  constexpr int kExports = 7;
+  constexpr int kExports = 9;
   IpcExport mine[kExports] = {export_pointer(send_ids.ptr), export_pointer(order.ptr),
                               export_pointer(loss_partials.ptr + gather_grid), exp_or_none(dense_dp.ptr),
-                              export_pointer(d_w), exp_or_none(d_state), exp_or_none(dense_flex.ptr)};
+                              export_pointer(d_w), exp_or_none(d_state), exp_or_none(dense_flex.ptr),
+                              exp_or_none(stamp_dp.ptr), exp_or_none(stamp_flex.ptr)};
   const std::vector<uint8_t> all = allgather_bytes(mine, sizeof(mine));
   peer_ids.assign(U, nullptr);
   peer_pos.assign(U, nullptr);
@@ -471,6 +486,10 @@ void ts_table::setup_p2p() {
   peer_state.assign(U, d_state);
   peer_dense_dp[g] = dense_dp.ptr;
   peer_dense_flex[g] = dense_flex.ptr;
+  peer_stamp_dp.assign(U, nullptr);
+  peer_stamp_flex.assign(U, nullptr);
+  peer_stamp_dp[g] = stamp_dp.ptr;
+  peer_stamp_flex[g] = stamp_flex.ptr;
   for (uint32_t p = 0; p < U; ++p) {
     if (p == g) continue;
     IpcExport e[kExports];
@@ -484,6 +503,8 @@ void ts_table::setup_p2p() {
     peer_w[p] = static_cast<float*>(peers.open(pp, e[4]));
     peer_state[p] = static_cast<float*>(open_opt(e[5]));
     peer_dense_flex[p] = static_cast<const float*>(open_opt(e[6]));
+    peer_stamp_dp[p] = static_cast<const uint32_t*>(open_opt(e[7]));
+    peer_stamp_flex[p] = static_cast<const uint32_t*>(open_opt(e[8]));
   }
   peer_grad.assign(U, nullptr);
   xfer.ensure(step_payload_bytes() * U);
@@ -887,14 +908,12 @@ void ts_table::backward_p2p(const float* d_grad) {
   TSD_CUDA(cudaEventRecord(ev_bwd0, stream));  // our gradient is complete here
   launch_build_entries(last_rows, order.ptr + n_remote, n_local_occ, rv, recv_ids.ptr, recv_before,
                        recv_total, static_cast<uint32_t>(occ), entry_keys.ptr, entry_vals.ptr, stream);
-  if (dp_rows) {
-    d0 = DenseRange{0, static_cast<uint32_t>(dp_rows), dense_dp.ptr};
-    TSD_CUDA(cudaMemsetAsync(dense_dp.ptr, 0, sizeof(float) * dp_rows * cfg.dim, stream));
-  }
+  // dense partials are stamped with the step's epoch instead of cleared
+  if (++epoch == 0) epoch = 1;  // (2^32 steps) 0 is the initial stamp
+  if (dp_rows) d0 = DenseRange{0, static_cast<uint32_t>(dp_rows), dense_dp.ptr, stamp_dp.ptr, epoch};
   if (N > 1 && flex_rows) {
     d1 = DenseRange{static_cast<uint32_t>(dp_rows), static_cast<uint32_t>(dp_rows + flex_rows),
-                    dense_flex.ptr};
-    TSD_CUDA(cudaMemsetAsync(dense_flex.ptr, 0, sizeof(float) * flex_rows * cfg.dim, stream));
+                    dense_flex.ptr, stamp_flex.ptr, epoch};
   }
   int t = phase_begin(kPhaseSort);
   radix_sort_pairs(entry_keys.ptr, entry_vals.ptr, m, bits_for(local_rows ? local_rows - 1 : 0), rb, &sk, &sv,
@@ -970,9 +989,11 @@ void ts_table::backward_p2p(const float* d_grad) {
     grp.row_lo = 0;
     for (uint32_t p = 0; p < U; ++p) {
       grp.grads[p] = peer_dense_dp[p];
+      grp.stamps[p] = peer_stamp_dp[p];
       grp.weights[p] = peer_w[p];
       grp.state[p] = peer_state[p];
     }
+    grp.epoch = epoch;
     launch_replica_update(grp, cfg.dim, opt, rs);
   }
   if (N > 1 && flex_rows) {
@@ -984,9 +1005,11 @@ void ts_table::backward_p2p(const float* d_grad) {
     for (uint32_t k = 0; k < N; ++k) {
       const uint32_t p = k * W + slot;
       grp.grads[k] = peer_dense_flex[p];
+      grp.stamps[k] = peer_stamp_flex[p];
       grp.weights[k] = peer_w[p] + dp_rows * cfg.dim;
       grp.state[k] = peer_state[p] ? peer_state[p] + dp_rows : nullptr;
     }
+    grp.epoch = epoch;
     launch_replica_update(grp, cfg.dim, opt, rs);
   }
   phase_end(t);
@@ -1018,6 +1041,7 @@ void ts_table::destroy() {
   d_loss.release();
   tier_counts.release();
   rows_dev.release();
+  host_out.release();
   sort_status.release();
   seg_split.release();
   seg_keys.release();
@@ -1027,6 +1051,8 @@ void ts_table::destroy() {
     b->release();
   }
   for (auto* b : {&partials, &send_rows, &recv_rows, &dense_dp, &dense_flex}) b->release();
+  stamp_dp.release();
+  stamp_flex.release();
   for (auto& [a, b] : ev_pool) {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
@@ -1112,15 +1138,19 @@ ts_status ts_table_train_step_host(ts_table* t, const uint32_t* h_rows, uint64_t
   return tsd::guarded([&] {
     if (!t || (occ && !h_rows)) tsd::fail(TS_ERR_CONFIG, "ts_table_train_step_host: null argument");
     TSD_CUDA(cudaSetDevice(t->cfg.device));
-    t->rows_dev.ensure(std::max<uint64_t>(occ, 1));
-    static thread_local tsd::DevBuf<float> out;  // per-thread scratch output
+    if (occ > t->cfg.max_occurrences) {
+      tsd::fail(TS_ERR_VALIDATION, "ts_table_train_step_host: occurrences exceed max_occurrences");
+    }
+    // sized once for the step cap: the output is peer-mapped by the other
+    // ranks, so it must not move between steps
+    t->rows_dev.ensure(t->cfg.max_occurrences);
+    t->host_out.ensure(t->cfg.max_occurrences * t->cfg.dim);
     if (occ) {
       TSD_CUDA(cudaMemcpyAsync(t->rows_dev.ptr, h_rows, sizeof(uint32_t) * occ, cudaMemcpyHostToDevice,
                                t->stream));
     }
-    out.ensure(std::max<uint64_t>(occ, 1) * t->cfg.dim);
-    t->forward(t->rows_dev.ptr, occ, out.ptr);
-    t->backward(out.ptr);
+    t->forward(t->rows_dev.ptr, occ, t->host_out.ptr);
+    t->backward(t->host_out.ptr);
     double loss = 0.0;
     TSD_CUDA(cudaMemcpyAsync(&loss, t->d_loss.ptr, sizeof(double), cudaMemcpyDeviceToHost, t->stream));
     TSD_CUDA(cudaStreamSynchronize(t->stream));

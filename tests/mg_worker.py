@@ -14,7 +14,10 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
 
-def problem(n_nodes, w, seed=11):
+def problem(n_nodes, w, seed=11, steps=1):
+    """rows[g] is rank g's first batch; steps > 1 adds steps_rows[s][g] for
+    the host-API multi-step case, batches growing step to step (so any
+    per-step buffer sized by the batch would have to move)."""
     import oracle_bind as orc
     u = n_nodes * w
     n, dim = 12000, 64
@@ -23,11 +26,14 @@ def problem(n_nodes, w, seed=11):
     p = np.arange(1, n + 1, dtype=np.float64) ** -1.1
     occ = [int(x) for x in rng.integers(3000, 6000, size=u)]
     rows = [rng.choice(n, size=o, p=p / p.sum()).astype(np.uint32) for o in occ]
+    steps_rows = [rows]
+    for s in range(1, steps):
+        steps_rows.append([rng.choice(n, size=o + 1500 * s, p=p / p.sum()).astype(np.uint32) for o in occ])
     tier, owner, slot = orc.assign_rows(np.zeros(n, np.uint32), np.arange(n, dtype=np.uint64),
                                         dp_cut, flex_cut, u, w, 2)
     dest = np.where(tier == 1, slot, owner).astype(np.uint8)
     return dict(n=n, dim=dim, dp_cut=dp_cut, flex_cut=flex_cut, rows=rows, tier=tier, owner=owner,
-                slot=slot, dest=dest)
+                slot=slot, dest=dest, steps_rows=steps_rows)
 
 
 def main():
@@ -36,6 +42,7 @@ def main():
     ap.add_argument("--gpus-per-node", type=int, required=True)
     ap.add_argument("--optimizer", type=int, default=1)
     ap.add_argument("--lr", type=float, default=1e-3)
+    ap.add_argument("--steps", type=int, default=1, help="> 1: host-buffer steps (train_step_host)")
     ap.add_argument("--out", required=True)
     args = ap.parse_args()
     import torch
@@ -48,21 +55,27 @@ def main():
     td.init_process_group("gloo")
     assert world == args.nodes * args.gpus_per_node
     torch.cuda.set_device(local)
-    pb = problem(args.nodes, args.gpus_per_node)
+    pb = problem(args.nodes, args.gpus_per_node, steps=args.steps)
     box = [ts.nccl_unique_id() if rank == 0 else None]
     td.broadcast_object_list(box, src=0)
     table = ts.Table(n_rows=pb["n"], dim=pb["dim"], dp_cut=pb["dp_cut"], flex_cut=pb["flex_cut"],
                      tier_dest=pb["dest"], num_nodes=args.nodes, gpus_per_node=args.gpus_per_node,
                      rank=rank, device=local, weight_seed=77, optimizer=args.optimizer, lr=args.lr,
-                     max_occurrences=int(pb["rows"][rank].size), nccl_unique_id=box[0])
-    rows = pb["rows"][rank]
-    d_rows = torch.from_numpy(rows.view(np.int32)).cuda()
-    d_out = torch.empty((rows.size, pb["dim"]), dtype=torch.float32, device="cuda")
-    table.forward(d_rows.data_ptr(), rows.size, d_out.data_ptr())
-    table.synchronize()
-    out = d_out.cpu().numpy().copy()
-    loss = table.loss()
-    table.backward(d_out.data_ptr())
+                     max_occurrences=int(max(r[rank].size for r in pb["steps_rows"])),
+                     nccl_unique_id=box[0])
+    if args.steps > 1:
+        losses = [table.train_step_host(r[rank]) for r in pb["steps_rows"]]
+        out = np.zeros((0, pb["dim"]), np.float32)
+        loss = np.array(losses)
+    else:
+        rows = pb["rows"][rank]
+        d_rows = torch.from_numpy(rows.view(np.int32)).cuda()
+        d_out = torch.empty((rows.size, pb["dim"]), dtype=torch.float32, device="cuda")
+        table.forward(d_rows.data_ptr(), rows.size, d_out.data_ptr())
+        table.synchronize()
+        out = d_out.cpu().numpy().copy()
+        loss = table.loss()
+        table.backward(d_out.data_ptr())
     table.synchronize()
     counters = table.counters()
     # rows stored on this rank

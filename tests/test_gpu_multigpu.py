@@ -44,13 +44,16 @@ def free_port():
 
 
 CASES = [(1, 2, 1, "p2p"), (2, 1, 1, "p2p"), (2, 1, 0, "p2p"), (2, 2, 1, "p2p"), (1, 4, 1, "p2p"),
+         (1, 2, 1, "p2p_peerload"), (2, 2, 1, "p2p_peerload"),
          (1, 2, 1, "nccl"), (2, 2, 1, "nccl"), (2, 1, 0, "nccl")]
 
 
 @pytest.mark.parametrize("n_nodes,w,opt,exchange", CASES)
 def test_multi_gpu_matches_oracle(cuda, tmp_path, n_nodes, w, opt, exchange):
-    """exchange: "p2p" = fused peer-memory gather/reads (default on one node),
-    "nccl" = staged NCCL all-to-allv (TIERSHARD_EXCHANGE=nccl)."""
+    """exchange: "p2p" = peer-memory serve + staged gradient pull (default on
+    one node), "p2p_peerload" = segment kernels load remote gradients from
+    peer memory (TIERSHARD_PULL_GRADS=0), "nccl" = staged NCCL all-to-allv
+    (TIERSHARD_EXCHANGE=nccl)."""
     u = n_nodes * w
     if n_devices() < u:
         pytest.skip(f"needs {u} GPUs")
@@ -58,7 +61,8 @@ def test_multi_gpu_matches_oracle(cuda, tmp_path, n_nodes, w, opt, exchange):
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
            str(ROOT / "tests" / "mg_worker.py"), "--nodes", str(n_nodes), "--gpus-per-node", str(w),
            "--optimizer", str(opt), "--lr", str(LR), "--out", str(tmp_path)]
-    env = dict(os.environ, TIERSHARD_EXCHANGE=exchange)
+    env = dict(os.environ, TIERSHARD_EXCHANGE="nccl" if exchange == "nccl" else "p2p",
+               TIERSHARD_PULL_GRADS="0" if exchange == "p2p_peerload" else "1")
     proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
     pb = mg_worker.problem(n_nodes, w)
@@ -94,5 +98,39 @@ def test_multi_gpu_matches_oracle(cuda, tmp_path, n_nodes, w, opt, exchange):
         if opt == 1:
             np.testing.assert_allclose(res[g]["state"], st_ref[stored], rtol=1e-5, atol=1e-12)
     # replicated DP rows are identical on every rank
+    for g in range(1, u):
+        assert np.array_equal(res[g]["weights"][:dp].view(np.uint32), res[0]["weights"][:dp].view(np.uint32))
+
+
+@pytest.mark.parametrize("n_nodes,w,opt", [(1, 2, 1), (2, 2, 1), (1, 4, 0)])
+def test_multi_gpu_host_steps_match_oracle(cuda, tmp_path, n_nodes, w, opt):
+    """Three steps through the host-buffer entry point (ts_table_train_step_host)
+    with batches growing step to step: every step's loss and the final weights
+    follow the oracle's sequential updates (stale peer mappings or stale
+    replica stamps would break this)."""
+    u = n_nodes * w
+    if n_devices() < u:
+        pytest.skip(f"needs {u} GPUs")
+    steps = 3
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={u}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           str(ROOT / "tests" / "mg_worker.py"), "--nodes", str(n_nodes), "--gpus-per-node", str(w),
+           "--optimizer", str(opt), "--lr", str(LR), "--steps", str(steps), "--out", str(tmp_path)]
+    proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
+    pb = mg_worker.problem(n_nodes, w, steps=steps)
+    res = [np.load(tmp_path / f"rank{g}.npz") for g in range(u)]
+    n, dim, dp, fx = pb["n"], pb["dim"], pb["dp_cut"], pb["flex_cut"]
+    w_ref = orc.init_table(77, n, dim)
+    st_ref = np.zeros(n, np.float32)
+    for s, batch in enumerate(pb["steps_rows"]):
+        allrows = np.concatenate(batch)
+        for g in range(u):  # each rank's loss: 0.5 |its unpooled rows|^2
+            expect = orc.half_sq_sum(orc.gather(w_ref, batch[g]))
+            assert float(res[g]["loss"][s]) == pytest.approx(expect, rel=1e-6), (s, g)
+        orc.backward_update(w_ref, st_ref, allrows, orc.gather(w_ref, allrows), opt, LR, 1e-8)
+    for g in range(u):
+        stored = res[g]["stored"]
+        np.testing.assert_allclose(res[g]["weights"], w_ref[stored], rtol=1e-5, atol=1e-8)
     for g in range(1, u):
         assert np.array_equal(res[g]["weights"][:dp].view(np.uint32), res[0]["weights"][:dp].view(np.uint32))
