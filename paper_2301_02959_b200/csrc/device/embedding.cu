@@ -934,6 +934,17 @@ void launch_segment_update(const uint32_t* keys, const uint32_t* vals, const uin
                                                             sc.long_list, sc.long_count);
     }
     TSD_LAUNCH_CHECK();
+  });
+}
+
+void launch_segment_long(const uint32_t* keys, const uint32_t* vals, const uint32_t* starts,
+                         uint64_t n_entries, uint32_t dim, const GradSource& grads, float* weights,
+                         float* state, const OptParams& opt, const DenseRange& dense0,
+                         const DenseRange& dense1, const SegmentScratch& sc, cudaStream_t stream) {
+  if (n_entries == 0) return;
+  const unsigned grid = persistent_grid(g_compute_blocks_per_sm);
+  dispatch_dim(dim, [&](auto D) {
+    constexpr int DIM = decltype(D)::value;
     long_prefix_kernel<<<1, 1024, 0, stream>>>(sc.long_list, sc.long_count, starts, sc.piece_off);
     TSD_LAUNCH_CHECK();
     piece_kernel<DIM><<<grid, kThreads, 0, stream>>>(vals, starts, sc.long_list, sc.long_count,

@@ -95,6 +95,13 @@ void launch_segment_update(const uint32_t* keys, const uint32_t* vals, const uin
                            float* state, const OptParams& opt, const DenseRange& dense0,
                            const DenseRange& dense1, const SegmentScratch& scratch,
                            cudaStream_t stream);
+// Second half of the segment update: segments longer than kPiece entries
+// that launch_segment_update listed (piece sums, then one combine per row).
+void launch_segment_long(const uint32_t* keys, const uint32_t* vals, const uint32_t* starts,
+                         uint64_t n_entries, uint32_t dim, const GradSource& grads, float* weights,
+                         float* state, const OptParams& opt, const DenseRange& dense0,
+                         const DenseRange& dense1, const SegmentScratch& scratch,
+                         cudaStream_t stream);
 
 // out[0] = 0, out[1] = number of segments whose key < split_key.
 void launch_segment_split(const uint32_t* keys, const uint32_t* starts, const uint32_t* d_nseg,

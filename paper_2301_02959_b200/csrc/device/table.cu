@@ -84,13 +84,14 @@ enum Phase : int {
   kPhaseAllReduce,
   kPhaseDenseUpdate,
   kPhaseReplicaUpdate,
+  kPhaseSegmentLong,
   kNumPhases
 };
 
 const char* const kPhaseNames[kNumPhases] = {
     "route",         "gather",         "exchange_fwd", "scatter",  "exchange_bwd",
     "dedup_sort",    "segment_starts", "segment_update", "allreduce", "dense_update",
-    "replica_update"};
+    "replica_update", "segment_long"};
 
 }  // namespace
 }  // namespace tsd
@@ -689,6 +690,9 @@ void ts_table::backward(const float* d_grad) {
     launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr, nseg.ptr, occ, cfg.dim, gs, d_w, d_state,
                           opt, d0, d1, sc, stream);
     phase_end(t);
+    t = phase_begin(kPhaseSegmentLong);
+    launch_segment_long(sk, sv, starts.ptr, occ, cfg.dim, gs, d_w, d_state, opt, d0, d1, sc, stream);
+    phase_end(t);
     return;
   }
 
@@ -747,6 +751,9 @@ void ts_table::backward(const float* d_grad) {
   launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr, seg_split.ptr + 1, m, cfg.dim, gs, d_w,
                         d_state, opt, d0, d1, sc, stream);
   phase_end(t);
+  t = phase_begin(kPhaseSegmentLong);
+  launch_segment_long(sk, sv, starts.ptr, m, cfg.dim, gs, d_w, d_state, opt, d0, d1, sc, stream);
+  phase_end(t);
   TSD_CUDA(cudaEventRecord(ev_dense, stream));
   TSD_CUDA(cudaStreamWaitEvent(comm, ev_dense, 0));
   t = phase_begin(kPhaseAllReduce, comm);
@@ -765,6 +772,9 @@ void ts_table::backward(const float* d_grad) {
   t = phase_begin(kPhaseSegmentUpdate);
   launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr + 1, nseg.ptr, m, cfg.dim, gs, d_w, d_state,
                         opt, d0, d1, sc, stream);
+  phase_end(t);
+  t = phase_begin(kPhaseSegmentLong);
+  launch_segment_long(sk, sv, starts.ptr, m, cfg.dim, gs, d_w, d_state, opt, d0, d1, sc, stream);
   phase_end(t);
   TSD_CUDA(cudaStreamWaitEvent(stream, ev_ar, 0));
   t = phase_begin(kPhaseDenseUpdate);
@@ -967,6 +977,9 @@ void ts_table::backward_p2p(const float* d_grad) {
   launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr, seg_split.ptr + 1, m, cfg.dim, gs, d_w, d_state,
                         opt, d0, d1, sc, stream);
   phase_end(t);
+  t = phase_begin(kPhaseSegmentLong);
+  launch_segment_long(sk, sv, starts.ptr, m, cfg.dim, gs, d_w, d_state, opt, d0, d1, sc, stream);
+  phase_end(t);
   // ---- replicated tiers over peer memory: after a rendezvous (all ranks'
   // partials written), each rank reduces its slice of the replicated rows in
   // group-rank order, updates it and broadcasts it to every replica --------
@@ -1017,6 +1030,9 @@ void ts_table::backward_p2p(const float* d_grad) {
   t = phase_begin(kPhaseSegmentUpdate);
   launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr + 1, nseg.ptr, m, cfg.dim, gs, d_w, d_state, opt,
                         d0, d1, sc, stream);
+  phase_end(t);
+  t = phase_begin(kPhaseSegmentLong);
+  launch_segment_long(sk, sv, starts.ptr, m, cfg.dim, gs, d_w, d_state, opt, d0, d1, sc, stream);
   phase_end(t);
   if (replica_concurrent) TSD_CUDA(cudaStreamWaitEvent(stream, ev_ar, 0));
   // peers store into our replicated rows: the next step's rendezvous (its
