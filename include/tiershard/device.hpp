@@ -11,6 +11,7 @@
 
 #include <array>
 #include <cstdint>
+#include <filesystem>
 #include <vector>
 
 #include "tiershard/cost_model.hpp"
@@ -19,7 +20,8 @@
 #include "tiershard/planner.hpp"
 #include "tiershard/topology.hpp"
 
-struct ts_table;  // C-ABI handle
+struct ts_table;   // C-ABI handles
+struct ts_keymap;
 
 namespace tiershard {
 
@@ -47,12 +49,55 @@ std::vector<uint8_t> placement_bytes(const ShardingPlan& plan, const RowDistribu
                                      const Topology& topo,
                                      uint64_t hash_seed = kDefaultPlacementSeed);
 
+// A plan imported from its on-disk artefacts (json_io.hpp): the plan
+// document (cuts, topology, cost model, hash seed, DP / Flex membership) and
+// the assignment CSV (every materialized row in canonical order with its
+// tier).  Together they determine every device remap table without the
+// distribution: canonical index = CSV line, tier = CSV column (checked
+// against the cuts and the document's dp_rows / flex_rows), placement byte =
+// row_key_hash(table, row, hash_seed) % U (RW) or % W (Flex), as assign_rows.
+struct DevicePlan {
+  ShardingPlan plan;  // dp_cut, flex_cut, total_rows, goal, predicted
+  Topology topology;
+  CostModelConfig cost_model;
+  uint64_t hash_seed = kDefaultPlacementSeed;
+  std::vector<uint32_t> table_ids;  // canonical order
+  std::vector<uint64_t> row_ids;
+  std::vector<uint8_t> placement;   // device placement byte per canonical row
+};
+
+// ConfigError on unreadable files; ValidationError when the CSV and the
+// document disagree (row count, tiers vs cuts, DP / Flex membership).
+DevicePlan load_device_plan(const std::filesystem::path& plan_json,
+                            const std::filesystem::path& assignment_csv);
+
+// Raw (table_id, row_id) keys -> canonical row indices on one GPU.
+class KeyMap {
+ public:
+  KeyMap(const std::vector<uint32_t>& table_ids, const std::vector<uint64_t>& row_ids, int device = 0);
+  explicit KeyMap(const DevicePlan& plan, int device = 0) : KeyMap(plan.table_ids, plan.row_ids, device) {}
+  ~KeyMap();
+  KeyMap(const KeyMap&) = delete;
+  KeyMap& operator=(const KeyMap&) = delete;
+
+  // Device pointers; absent keys map to 0xFFFFFFFF.  Returns the number of
+  // absent keys (synchronises the stream; nullptr = the map's own stream).
+  uint64_t lookup(const uint32_t* d_table_ids, const uint64_t* d_row_ids, uint64_t n,
+                  uint32_t* d_canon, void* stream = nullptr) const;
+  ts_keymap* handle() const { return map_; }
+
+ private:
+  ts_keymap* map_ = nullptr;
+};
+
 // One rank's shard of the tiered table.  Collective when N*W > 1.
 class SequenceEmbedding {
  public:
   SequenceEmbedding(const ShardingPlan& plan, const RowDistribution& dist, const Topology& topo,
                     const CostModelConfig& cfg, const DeviceOptions& options,
                     uint64_t hash_seed = kDefaultPlacementSeed);
+  // From an imported plan (topology, cost model and placement included).
+  SequenceEmbedding(const DevicePlan& plan, const DeviceOptions& options);
   ~SequenceEmbedding();
   SequenceEmbedding(const SequenceEmbedding&) = delete;
   SequenceEmbedding& operator=(const SequenceEmbedding&) = delete;
@@ -60,6 +105,10 @@ class SequenceEmbedding {
   // Lookup: d_rows (device) holds this rank's occurrences as canonical row
   // indices; d_out (device) receives the unpooled [occurrences x D] rows.
   void forward(const uint32_t* d_rows, uint64_t occurrences, float* d_out);
+  // Same with raw keys (device pointers), looked up through `keys`;
+  // ValidationError when a key is absent from the plan.
+  void forward_keys(const KeyMap& keys, const uint32_t* d_table_ids, const uint64_t* d_row_ids,
+                    uint64_t occurrences, float* d_out);
   // Update for the last forward from d_grad [occurrences x D] (device).
   void backward(const float* d_grad);
   // Host-buffer step: copy, forward, loss 0.5*|out|^2, backward, read loss.
@@ -76,6 +125,8 @@ class SequenceEmbedding {
   uint32_t dim() const { return dim_; }
 
  private:
+  void create(uint64_t n_rows, uint64_t dp_cut, uint64_t flex_cut, const std::vector<uint8_t>& dest,
+              const Topology& topo, const CostModelConfig& cfg, const DeviceOptions& options);
   ts_table* table_ = nullptr;
   uint32_t dim_ = 0;
   uint32_t gpus_ = 1;

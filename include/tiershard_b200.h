@@ -113,6 +113,31 @@ ts_status ts_router_iteration_device(ts_router* r, const uint64_t* d_requester_b
 ts_status ts_router_destroy(ts_router* r);
 
 /* ------------------------------------------------------------------------
+ * Key map: raw (table_id, row_id) keys -> canonical row index (the u32 the
+ * router and the table consume), for inputs that arrive as raw ids: the
+ * reference names rows by (table_id, row_id) in RowRecord
+ * (distribution.hpp:31-38), in the plan document's dp_rows / flex_rows and
+ * in the assignment CSV (json_io.cpp:235-244, 380-394).
+ * ---------------------------------------------------------------------- */
+typedef struct ts_keymap ts_keymap;
+
+/* Uploads the canonical order: row i of the plan is (table_ids[i],
+ * row_ids[i]).  ValidationError on duplicate keys; ConfigError when table
+ * ids reach 2^24 or row ids are too sparse for the dense map. */
+ts_status ts_keymap_create(ts_keymap** out, int device, uint64_t n_rows,
+                           const uint32_t* table_ids, const uint64_t* row_ids);
+
+/* d_canon[i] = canonical index of (d_table_ids[i], d_row_ids[i]), or
+ * 0xFFFFFFFF for keys absent from the plan (all device pointers; stream NULL
+ * = the map's own stream).  With misses != NULL the call synchronises and
+ * stores the number of absent keys. */
+ts_status ts_keymap_lookup(ts_keymap* m, const uint32_t* d_table_ids,
+                           const uint64_t* d_row_ids, uint64_t n, uint32_t* d_canon,
+                           void* stream, uint64_t* misses);
+
+ts_status ts_keymap_destroy(ts_keymap* m);
+
+/* ------------------------------------------------------------------------
  * Host-only planning helpers of the U > 1 path (no device needed).
  * ---------------------------------------------------------------------- */
 
@@ -226,6 +251,14 @@ const char* ts_table_phase_name(int phase);
  * from the first recorded event.  Synchronises the table's streams. */
 ts_status ts_table_phase_trace(ts_table* t, int* phase, int* stream_id, double* t0_ms,
                                double* t1_ms, int capacity, int* count);
+
+/* ts_table_forward with raw (table_id, row_id) keys (ts_keymap above): the
+ * lookup runs on the table's stream into the map's scratch (valid until the
+ * next call, so the following ts_table_backward sees the same ids), then the
+ * forward.  Synchronises once to reject absent keys (ValidationError) before
+ * any row is read. */
+ts_status ts_table_forward_keys(ts_table* t, ts_keymap* m, const uint32_t* d_table_ids,
+                                const uint64_t* d_row_ids, uint64_t occurrences, float* d_out);
 
 #ifdef __cplusplus
 }

@@ -11,6 +11,7 @@ from .capi import (  # noqa: F401
     DRIVER_PATH,
     TSError,
     Router,
+    KeyMap,
     Table,
     load,
     build_info,

@@ -68,6 +68,10 @@ EXPORTS = (
     "ts_table_phase_times",
     "ts_table_phase_name",
     "ts_table_phase_trace",
+    "ts_keymap_create",
+    "ts_keymap_lookup",
+    "ts_keymap_destroy",
+    "ts_table_forward_keys",
 )
 
 
@@ -150,6 +154,10 @@ def load() -> C.CDLL:
         "ts_table_phase_times": (C.c_int, [vp, f64p, u64p, C.c_int, C.POINTER(C.c_int)]),
         "ts_table_phase_name": (C.c_char_p, [C.c_int]),
         "ts_table_phase_trace": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.POINTER(C.c_int)]),
+        "ts_keymap_create": (C.c_int, [C.POINTER(vp), C.c_int, C.c_uint64, vp, vp]),
+        "ts_keymap_lookup": (C.c_int, [vp, vp, vp, C.c_uint64, vp, vp, u64p]),
+        "ts_keymap_destroy": (C.c_int, [vp]),
+        "ts_table_forward_keys": (C.c_int, [vp, vp, vp, vp, C.c_uint64, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -248,6 +256,42 @@ class Router:
             pass
 
 
+class KeyMap:
+    """ts_keymap_*: raw (table_id, row_id) -> canonical row index on the device."""
+
+    ABSENT = 0xFFFFFFFF
+
+    def __init__(self, table_ids: np.ndarray, row_ids: np.ndarray, device: int = 0):
+        self._lib = load()
+        t = np.ascontiguousarray(table_ids, dtype=np.uint32)
+        r = np.ascontiguousarray(row_ids, dtype=np.uint64)
+        assert t.shape == r.shape
+        h = vp()
+        _check(self._lib.ts_keymap_create(C.byref(h), device, t.size, _ptr(t) if t.size else None,
+                                          _ptr(r) if r.size else None))
+        self._h = h
+
+    def lookup_device(self, d_table_ids: int, d_row_ids: int, n: int, d_canon: int,
+                      stream: int = 0, count_misses: bool = True):
+        """Device pointers in and out; returns the miss count (synchronises) or None."""
+        m = C.c_uint64(0)
+        _check(self._lib.ts_keymap_lookup(self._h, d_table_ids or None, d_row_ids or None, n,
+                                          d_canon or None, stream or None,
+                                          C.byref(m) if count_misses else None))
+        return m.value if count_misses else None
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _check(self._lib.ts_keymap_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Table:
     """ts_table_*: one rank's shard with lookup (forward) and update (backward)."""
 
@@ -277,6 +321,10 @@ class Table:
     # --- device-pointer entry points -------------------------------------
     def forward(self, d_rows: int, occ: int, d_out: int) -> None:
         _check(self._lib.ts_table_forward(self._h, d_rows, occ, d_out))
+
+    def forward_keys(self, keymap: "KeyMap", d_table_ids: int, d_row_ids: int, occ: int,
+                     d_out: int) -> None:
+        _check(self._lib.ts_table_forward_keys(self._h, keymap._h, d_table_ids, d_row_ids, occ, d_out))
 
     def backward(self, d_grad: int) -> None:
         _check(self._lib.ts_table_backward(self._h, d_grad))

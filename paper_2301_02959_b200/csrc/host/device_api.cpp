@@ -32,21 +32,36 @@ std::vector<uint8_t> placement_bytes(const ShardingPlan& plan, const RowDistribu
 
 SequenceEmbedding::SequenceEmbedding(const ShardingPlan& plan, const RowDistribution& dist,
                                      const Topology& topo, const CostModelConfig& cfg,
-                                     const DeviceOptions& options, uint64_t hash_seed)
-    : dim_(cfg.embedding_dim), gpus_(topo.total_gpus()) {
+                                     const DeviceOptions& options, uint64_t hash_seed) {
   cfg.validate();
   topo.validate();
+  create(dist.rows().size(), plan.dp_cut, plan.flex_cut, placement_bytes(plan, dist, topo, hash_seed),
+         topo, cfg, options);
+}
+
+SequenceEmbedding::SequenceEmbedding(const DevicePlan& plan, const DeviceOptions& options) {
+  plan.cost_model.validate();
+  plan.topology.validate();
+  create(plan.table_ids.size(), plan.plan.dp_cut, plan.plan.flex_cut, plan.placement, plan.topology,
+         plan.cost_model, options);
+}
+
+void SequenceEmbedding::create(uint64_t n_rows, uint64_t dp_cut, uint64_t flex_cut,
+                               const std::vector<uint8_t>& dest, const Topology& topo,
+                               const CostModelConfig& cfg, const DeviceOptions& options) {
   if (cfg.scalar_bytes != 4) throw ConfigError("device path: fp32 tables only (scalar_bytes = 4)");
-  const std::vector<uint8_t> dest = placement_bytes(plan, dist, topo, hash_seed);
+  if (dest.size() != n_rows) throw ValidationError("device path: placement does not cover the rows");
+  dim_ = cfg.embedding_dim;
+  gpus_ = topo.total_gpus();
   ts_table_config c{};
   c.num_nodes = topo.num_nodes;
   c.gpus_per_node = topo.gpus_per_node;
   c.rank = options.rank;
   c.device = options.device;
   c.dim = cfg.embedding_dim;
-  c.n_rows = dist.rows().size();
-  c.dp_cut = plan.dp_cut;
-  c.flex_cut = plan.flex_cut;
+  c.n_rows = n_rows;
+  c.dp_cut = dp_cut;
+  c.flex_cut = flex_cut;
   c.weight_seed = options.weight_seed;
   c.optimizer = options.optimizer == Optimizer::kSgd ? TS_OPT_SGD : TS_OPT_ROWWISE_ADAGRAD;
   c.lr = options.learning_rate;
@@ -62,6 +77,27 @@ SequenceEmbedding::~SequenceEmbedding() {
 
 void SequenceEmbedding::forward(const uint32_t* d_rows, uint64_t occurrences, float* d_out) {
   detail::check(ts_table_forward(table_, d_rows, occurrences, d_out));
+}
+
+void SequenceEmbedding::forward_keys(const KeyMap& keys, const uint32_t* d_table_ids,
+                                     const uint64_t* d_row_ids, uint64_t occurrences, float* d_out) {
+  detail::check(ts_table_forward_keys(table_, keys.handle(), d_table_ids, d_row_ids, occurrences, d_out));
+}
+
+KeyMap::KeyMap(const std::vector<uint32_t>& table_ids, const std::vector<uint64_t>& row_ids, int device) {
+  if (table_ids.size() != row_ids.size()) throw ConfigError("KeyMap: table_ids / row_ids size mismatch");
+  detail::check(ts_keymap_create(&map_, device, table_ids.size(), table_ids.data(), row_ids.data()));
+}
+
+KeyMap::~KeyMap() {
+  if (map_) ts_keymap_destroy(map_);
+}
+
+uint64_t KeyMap::lookup(const uint32_t* d_table_ids, const uint64_t* d_row_ids, uint64_t n,
+                        uint32_t* d_canon, void* stream) const {
+  uint64_t misses = 0;
+  detail::check(ts_keymap_lookup(map_, d_table_ids, d_row_ids, n, d_canon, stream, &misses));
+  return misses;
 }
 
 void SequenceEmbedding::backward(const float* d_grad) { detail::check(ts_table_backward(table_, d_grad)); }

@@ -4,17 +4,95 @@
 // through tiershard/device.hpp.  Prints one JSON line.
 //
 // Usage: ts_example [rows] [dim] [batch] [steps]
+//        ts_example --plan PLAN.json ASSIGNMENT.csv [steps]
+//   The second form imports a plan from the reference's on-disk formats
+//   (load_device_plan) and feeds raw (table_id, row_id) keys through a
+//   KeyMap; it runs the table on one GPU (topology collapsed to 1 x 1, every
+//   tier local) -- a U-GPU job keeps the plan's topology, one rank per process.
+#include <cuda_runtime.h>
+
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <memory>
+#include <random>
 
 #include "tiershard/device.hpp"
 #include "tiershard/error.hpp"
 #include "tiershard/planner.hpp"
 #include "tiershard/simulator.hpp"
 
+namespace {
+
+int run_from_plan(const char* plan_json, const char* assignment_csv, int steps) {
+  namespace ts = tiershard;
+  ts::DevicePlan dp = ts::load_device_plan(plan_json, assignment_csv);
+  dp.topology.num_nodes = 1;  // one GPU: every tier local
+  dp.topology.gpus_per_node = 1;
+  dp.topology.a2a_global = dp.topology.a2a_intra = dp.topology.ar_global = dp.topology.ar_cross = ts::kGiB;
+  std::fill(dp.placement.begin(), dp.placement.end(), 0);
+  const uint64_t n = dp.table_ids.size();
+  const uint64_t occ = uint64_t{dp.cost_model.local_batch} * 16;
+  ts::DeviceOptions opt;
+  opt.max_occurrences = occ;
+  ts::SequenceEmbedding table(dp, opt);
+  ts::KeyMap keys(dp);
+  std::mt19937_64 rng(17);
+  std::vector<uint32_t> h_t(occ);
+  std::vector<uint64_t> h_r(occ);
+  uint32_t* d_t = nullptr;
+  uint64_t* d_r = nullptr;
+  float* d_out = nullptr;
+  const auto ok = [](cudaError_t e) {
+    if (e != cudaSuccess) throw ts::Error(std::string("cuda: ") + cudaGetErrorString(e));
+  };
+  ok(cudaMalloc(&d_t, sizeof(uint32_t) * occ));
+  ok(cudaMalloc(&d_r, sizeof(uint64_t) * occ));
+  ok(cudaMalloc(&d_out, sizeof(float) * occ * table.dim()));
+  double loss = 0.0;
+  for (int s = 0; s < steps; ++s) {
+    for (uint64_t i = 0; i < occ; ++i) {  // raw keys of plan rows, hot rows first-weighted
+      const uint64_t k = (rng() % n) * (rng() % n) / n;
+      h_t[i] = dp.table_ids[k];
+      h_r[i] = dp.row_ids[k];
+    }
+    ok(cudaMemcpy(d_t, h_t.data(), sizeof(uint32_t) * occ, cudaMemcpyHostToDevice));
+    ok(cudaMemcpy(d_r, h_r.data(), sizeof(uint64_t) * occ, cudaMemcpyHostToDevice));
+    table.forward_keys(keys, d_t, d_r, occ, d_out);
+    table.backward(d_out);  // grad = out: loss 0.5 |out|^2
+    table.synchronize();
+    std::vector<float> h_out(occ * table.dim());
+    ok(cudaMemcpy(h_out.data(), d_out, sizeof(float) * h_out.size(), cudaMemcpyDeviceToHost));
+    loss = 0.0;
+    for (float v : h_out) loss += 0.5 * double(v) * double(v);
+  }
+  cudaFree(d_t);
+  cudaFree(d_r);
+  cudaFree(d_out);
+  std::printf("{\"rows\": %llu, \"dp_cut\": %llu, \"flex_cut\": %llu, \"occurrences\": %llu, "
+              "\"last_loss\": %.17g}\n",
+              static_cast<unsigned long long>(n), static_cast<unsigned long long>(dp.plan.dp_cut),
+              static_cast<unsigned long long>(dp.plan.flex_cut),
+              static_cast<unsigned long long>(occ * steps), loss);
+  return 0;
+}
+
+}  // namespace
+
 int main(int argc, char** argv) {
   namespace ts = tiershard;
+  if (argc > 1 && std::strcmp(argv[1], "--plan") == 0) {
+    if (argc < 4) {
+      std::fprintf(stderr, "usage: %s --plan PLAN.json ASSIGNMENT.csv [steps]\n", argv[0]);
+      return 2;
+    }
+    try {
+      return run_from_plan(argv[2], argv[3], argc > 4 ? std::atoi(argv[4]) : 3);
+    } catch (const ts::Error& e) {
+      std::printf("{\"error\": \"%s\"}\n", e.what());
+      return 3;
+    }
+  }
   const uint64_t rows = argc > 1 ? std::strtoull(argv[1], nullptr, 10) : 100000;
   const uint32_t dim = argc > 2 ? static_cast<uint32_t>(std::atoi(argv[2])) : 64;
   const uint32_t batch = argc > 3 ? static_cast<uint32_t>(std::atoi(argv[3])) : 128;
