@@ -367,6 +367,22 @@ def run_ours(args, dist: Dist):
                 table.train_step(b.data_ptr(), b.numel(), d_out.data_ptr())
                 table.loss()
             e2e["diag_torch_buffers_value"] = samples / dist.max(time.perf_counter() - t1)
+            views = [t.numpy().view(np.uint32) for t in pin_t]  # tensors stay referenced by pin_t
+            dist.barrier()
+            t1 = time.perf_counter()
+            for k in range(args.steps):
+                table.train_step_host(views[k % len(views)])
+            e2e["diag_host_api_pinned_value"] = samples / dist.max(time.perf_counter() - t1)
+            import ctypes
+            hostmem = []
+            for k in range(min(2, len(batches))):
+                flags = ctypes.c_uint(0)
+                rc = torch.cuda.cudart().cudaHostGetFlags(ctypes.byref(flags), pinned[k].ctypes.data) \
+                    if hasattr(torch.cuda.cudart(), "cudaHostGetFlags") else None
+                hostmem.append(str(rc))
+            e2e["diag_pinned_check"] = hostmem
+            torch.cuda.synchronize()
+            del views
             torch.cuda.synchronize()
             del pin_t  # pinned blocks carry events on the table's stream: free before it goes
         # one more host-buffer step with the phase timeline (diagnostics)

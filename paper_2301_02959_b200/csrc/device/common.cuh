@@ -105,6 +105,21 @@ __device__ __forceinline__ void stg_stream(float4* p, float4 v) {
 
 inline unsigned ceil_div(uint64_t a, uint64_t b) { return static_cast<unsigned>((a + b - 1) / b); }
 
+// cudaMalloc rounded up to whole 2 MiB pages for anything over 1 MiB.
+// Measured on B200: a 2.0003 GiB buffer whose size was not a 2 MiB multiple
+// made every NVLink access to it (peer stores into it, peer loads from it)
+// about 2x slower than the same buffer rounded up (U = 4 host-buffer step
+// 5.9 -> 3.9 ms), consistent with the allocation falling back to small pages.
+inline cudaError_t dev_alloc(void** p, uint64_t bytes) {
+  constexpr uint64_t kPage = uint64_t{2} << 20;
+  if (bytes > (kPage >> 1)) bytes = (bytes + kPage - 1) / kPage * kPage;
+  return cudaMalloc(p, bytes);
+}
+template <typename T>
+inline cudaError_t dev_alloc(T** p, uint64_t bytes) {
+  return dev_alloc(reinterpret_cast<void**>(p), bytes);
+}
+
 // Number of SMs on the current device (cached per device).
 int sm_count();
 

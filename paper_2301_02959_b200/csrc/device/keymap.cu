@@ -128,9 +128,9 @@ ts_status ts_keymap_create(ts_keymap** out, int device, uint64_t n_rows, const u
     m->n_dir = n_dir;
     try {
       TSD_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
-      TSD_CUDA(cudaMalloc(&m->d_dir, sizeof(TableDir) * std::max<uint32_t>(n_dir, 1)));
-      TSD_CUDA(cudaMalloc(&m->d_slots, sizeof(uint32_t) * std::max<uint64_t>(total, 1)));
-      TSD_CUDA(cudaMalloc(&m->d_count, sizeof(unsigned long long)));
+      TSD_CUDA(dev_alloc(&m->d_dir, sizeof(TableDir) * std::max<uint32_t>(n_dir, 1)));
+      TSD_CUDA(dev_alloc(&m->d_slots, sizeof(uint32_t) * std::max<uint64_t>(total, 1)));
+      TSD_CUDA(dev_alloc(&m->d_count, sizeof(unsigned long long)));
       TSD_CUDA(cudaMemsetAsync(m->d_slots, 0xFF, sizeof(uint32_t) * std::max<uint64_t>(total, 1), m->stream));
       TSD_CUDA(cudaMemsetAsync(m->d_count, 0, sizeof(unsigned long long), m->stream));
       if (n_rows) {
@@ -138,8 +138,8 @@ ts_status ts_keymap_create(ts_keymap** out, int device, uint64_t n_rows, const u
                                  m->stream));
         uint32_t* d_t = nullptr;
         uint64_t* d_r = nullptr;
-        TSD_CUDA(cudaMalloc(&d_t, sizeof(uint32_t) * n_rows));
-        TSD_CUDA(cudaMalloc(&d_r, sizeof(uint64_t) * n_rows));
+        TSD_CUDA(dev_alloc(&d_t, sizeof(uint32_t) * n_rows));
+        TSD_CUDA(dev_alloc(&d_r, sizeof(uint64_t) * n_rows));
         TSD_CUDA(cudaMemcpyAsync(d_t, table_ids, sizeof(uint32_t) * n_rows, cudaMemcpyHostToDevice, m->stream));
         TSD_CUDA(cudaMemcpyAsync(d_r, row_ids, sizeof(uint64_t) * n_rows, cudaMemcpyHostToDevice, m->stream));
         const unsigned grid = std::max(1u, std::min<unsigned>(ceil_div(n_rows, kThreads), 8 * sm_count()));
@@ -202,7 +202,7 @@ ts_status ts_table_forward_keys(ts_table* t, ts_keymap* m, const uint32_t* d_tab
       cudaFree(m->d_canon);
       m->d_canon = nullptr;
       m->canon_cap = 0;
-      TSD_CUDA(cudaMalloc(&m->d_canon, sizeof(uint32_t) * occ));
+      TSD_CUDA(dev_alloc(&m->d_canon, sizeof(uint32_t) * occ));
       m->canon_cap = occ;
     }
     uint64_t misses = 0;

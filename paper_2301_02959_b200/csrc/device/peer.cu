@@ -2,6 +2,8 @@
 #include <cuda.h>
 #include <dlfcn.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -175,6 +177,7 @@ void* PeerMappings::open(int peer, const IpcExport& e) {
   const auto key = std::make_pair(peer, e.base_id);
   auto it = opened_.find(key);
   if (it != opened_.end() && std::memcmp(&it->second.handle, &e.handle, sizeof(e.handle)) != 0) {
+    ++reopens_;
     TSD_CUDA(cudaIpcCloseMemHandle(it->second.base));
     opened_.erase(it);
     it = opened_.end();
@@ -182,12 +185,17 @@ void* PeerMappings::open(int peer, const IpcExport& e) {
   if (it == opened_.end()) {
     void* p = nullptr;
     TSD_CUDA(cudaIpcOpenMemHandle(&p, e.handle, cudaIpcMemLazyEnablePeerAccess));
+    ++opens_;
     it = opened_.emplace(key, Mapping{e.handle, p}).first;
   }
   return static_cast<char*>(it->second.base) + e.offset;
 }
 
 void PeerMappings::close_all() {
+  if (std::getenv("TIERSHARD_DEBUG_IPC") && opens_) {
+    std::fprintf(stderr, "tiershard: peer mappings: %llu opens, %llu handle changes\n",
+                 static_cast<unsigned long long>(opens_), static_cast<unsigned long long>(reopens_));
+  }
   for (auto& kv : opened_) cudaIpcCloseMemHandle(kv.second.base);
   opened_.clear();
 }

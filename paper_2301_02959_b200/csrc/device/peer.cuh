@@ -51,6 +51,7 @@ class PeerMappings {
     void* base;
   };
   std::map<std::pair<int, uint64_t>, Mapping> opened_;  // (peer, base_id) -> mapping
+  uint64_t opens_ = 0, reopens_ = 0;
 };
 
 // Request lists a server pulls: for each source rank, a run of `count`

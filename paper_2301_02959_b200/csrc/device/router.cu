@@ -177,11 +177,11 @@ ts_status ts_router_create(ts_router** out, int device, uint64_t n_rows, uint64_
     r->gpus_per_node = gpus_per_node;
     r->seen_words = (n_rows + 31) / 32;
     TSD_CUDA(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
-    TSD_CUDA(cudaMalloc(&r->d_dest, n_rows));
-    TSD_CUDA(cudaMalloc(&r->d_seen, sizeof(uint32_t) * r->seen_words * u));
-    TSD_CUDA(cudaMalloc(&r->d_counters, sizeof(unsigned long long) * TS_NUM_COUNTERS * u));
-    TSD_CUDA(cudaMalloc(&r->d_bad, sizeof(unsigned)));
-    TSD_CUDA(cudaMalloc(&r->d_bounds, sizeof(uint64_t) * (u + 1)));
+    TSD_CUDA(dev_alloc(&r->d_dest, n_rows));
+    TSD_CUDA(dev_alloc(&r->d_seen, sizeof(uint32_t) * r->seen_words * u));
+    TSD_CUDA(dev_alloc(&r->d_counters, sizeof(unsigned long long) * TS_NUM_COUNTERS * u));
+    TSD_CUDA(dev_alloc(&r->d_bad, sizeof(unsigned)));
+    TSD_CUDA(dev_alloc(&r->d_bounds, sizeof(uint64_t) * (u + 1)));
     TSD_CUDA(cudaMemcpy(r->d_dest, tier_dest, n_rows, cudaMemcpyHostToDevice));
     // validate placement bytes against U / W once, on the host copy
     for (uint64_t i = dp_cut; i < n_rows; ++i) {
@@ -209,7 +209,7 @@ ts_status ts_router_iteration(ts_router* r, uint32_t local_batch, const uint64_t
       if (r->d_rows) TSD_CUDA(cudaFree(r->d_rows));
       r->d_rows = nullptr;
       r->rows_capacity = occurrences + occurrences / 8;
-      TSD_CUDA(cudaMalloc(&r->d_rows, sizeof(uint32_t) * r->rows_capacity));
+      TSD_CUDA(dev_alloc(&r->d_rows, sizeof(uint32_t) * r->rows_capacity));
     }
     TSD_CUDA(cudaMemcpyAsync(r->d_bounds, bounds.data(), sizeof(uint64_t) * (U + 1),
                              cudaMemcpyHostToDevice, r->stream));

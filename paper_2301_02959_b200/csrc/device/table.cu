@@ -56,8 +56,12 @@ struct DevBuf {
     if (n <= cap && ptr) return;
     if (ptr) TSD_CUDA(cudaFree(ptr));
     ptr = nullptr;
-    cap = std::max<uint64_t>(n, 1);
-    TSD_CUDA(cudaMalloc(&ptr, sizeof(T) * cap));
+    // whole 2 MiB pages (dev_alloc): the spare tail becomes capacity
+    constexpr uint64_t kPage = uint64_t{2} << 20;
+    uint64_t bytes = sizeof(T) * std::max<uint64_t>(n, 1);
+    if (bytes > (kPage >> 1)) bytes = (bytes + kPage - 1) / kPage * kPage;
+    cap = bytes / sizeof(T);
+    TSD_CUDA(dev_alloc(&ptr, bytes));
   }
   void release() {
     if (ptr) cudaFree(ptr);
@@ -336,16 +340,16 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     for (uint64_t i = c.flex_cut; i < n; ++i) {
       if (tier_dest[i] == g) l2c[h_local[i]] = static_cast<uint32_t>(i);
     }
-    TSD_CUDA(cudaMalloc(&d_dest, n));
-    TSD_CUDA(cudaMalloc(&d_local, sizeof(uint32_t) * n));
+    TSD_CUDA(dev_alloc(&d_dest, n));
+    TSD_CUDA(dev_alloc(&d_local, sizeof(uint32_t) * n));
     TSD_CUDA(cudaMemcpyAsync(d_dest, tier_dest, n, cudaMemcpyHostToDevice, stream));
     TSD_CUDA(cudaMemcpyAsync(d_local, h_local.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice,
                              stream));
   }
 
-  TSD_CUDA(cudaMalloc(&d_w, sizeof(float) * std::max<uint64_t>(local_rows, 1) * c.dim));
+  TSD_CUDA(dev_alloc(&d_w, sizeof(float) * std::max<uint64_t>(local_rows, 1) * c.dim));
   if (c.optimizer == TS_OPT_ROWWISE_ADAGRAD) {
-    TSD_CUDA(cudaMalloc(&d_state, sizeof(float) * std::max<uint64_t>(local_rows, 1)));
+    TSD_CUDA(dev_alloc(&d_state, sizeof(float) * std::max<uint64_t>(local_rows, 1)));
     TSD_CUDA(cudaMemsetAsync(d_state, 0, sizeof(float) * std::max<uint64_t>(local_rows, 1), stream));
   }
   {

@@ -11,6 +11,10 @@ all-reduce sums a replicated row's gradient in a different fp32 order than the
 single-process oracle (~sqrt(n) ulps apart for n occurrences), and that
 difference reaches the weight scaled by lr * |step| / |w|."""
 LR = 1e-3
+# multi-step runs feed each step's weights into the next step's gradients
+# (grad = out); a smaller rate keeps SGD on the hottest rows contractive so the
+# summation-order differences do not compound across steps
+LR_STEPS = 1e-4
 import os
 import socket
 import subprocess
@@ -115,7 +119,7 @@ def test_multi_gpu_host_steps_match_oracle(cuda, tmp_path, n_nodes, w, opt):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={u}",
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
            str(ROOT / "tests" / "mg_worker.py"), "--nodes", str(n_nodes), "--gpus-per-node", str(w),
-           "--optimizer", str(opt), "--lr", str(LR), "--steps", str(steps), "--out", str(tmp_path)]
+           "--optimizer", str(opt), "--lr", str(LR_STEPS), "--steps", str(steps), "--out", str(tmp_path)]
     proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
     pb = mg_worker.problem(n_nodes, w, steps=steps)
@@ -128,9 +132,9 @@ def test_multi_gpu_host_steps_match_oracle(cuda, tmp_path, n_nodes, w, opt):
         for g in range(u):  # each rank's loss: 0.5 |its unpooled rows|^2
             expect = orc.half_sq_sum(orc.gather(w_ref, batch[g]))
             assert float(res[g]["loss"][s]) == pytest.approx(expect, rel=1e-6), (s, g)
-        orc.backward_update(w_ref, st_ref, allrows, orc.gather(w_ref, allrows), opt, LR, 1e-8)
+        orc.backward_update(w_ref, st_ref, allrows, orc.gather(w_ref, allrows), opt, LR_STEPS, 1e-8)
     for g in range(u):
         stored = res[g]["stored"]
-        np.testing.assert_allclose(res[g]["weights"], w_ref[stored], rtol=1e-5, atol=1e-8)
+        np.testing.assert_allclose(res[g]["weights"], w_ref[stored], rtol=1e-6, atol=1e-9)
     for g in range(1, u):
         assert np.array_equal(res[g]["weights"][:dp].view(np.uint32), res[0]["weights"][:dp].view(np.uint32))
