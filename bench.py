@@ -100,6 +100,14 @@ class Dist:
         self.td.all_reduce(t, op=self.td.ReduceOp.SUM)
         return float(t.item())
 
+    def gather(self, obj):
+        """All ranks' objects, in rank order (every rank gets the list)."""
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        self.td.all_gather_object(out, obj)
+        return out
+
     def bcast(self, obj):
         if self.world == 1:
             return obj
@@ -335,6 +343,7 @@ def run_ours(args, dist: Dist):
     phases = table.phase_times()
     step(prof_steps)  # one more step: its timeline (both streams)
     trace = [(n, sid, round(a, 4), round(b, 4)) for n, sid, a, b in table.phase_trace()]
+    all_traces = dist.gather(trace) if os.environ.get("TS_BENCH_DIAG") else None
     table.enable_timing(False)
 
     # ---- end to end through the host-buffer public entry point -------------
@@ -454,6 +463,30 @@ def run_ours(args, dist: Dist):
         "plan_off_device_GB": (off_dev["plan_global_bytes"] + off_dev["plan_intra_bytes"]) / 1e9,
     }
 
+    # ---- NVLink roofline (U > 1): bytes each GPU must move per step, one
+    # direction: its share of the off-device row traffic for the forward rows
+    # and the backward gradients (2 passes), plus the replicated tiers'
+    # reduce + broadcast, 2 (G-1)/G x replicated rows x row_bytes per group
+    # of G (the all-reduce volume); over the measured step
+    # time, against the measured peer-copy bandwidth (B200_PROFILING.md).
+    nvlink = None
+    if u > 1:
+        n_nodes = u // w
+        flex_slot_rows = (plan["flex_cut"] - plan["dp_cut"]) / w
+        per_gpu = {
+            "rows_fwd_bwd": 2 * (off_dev["plan_global_bytes"] + off_dev["plan_intra_bytes"]) / u,
+            "replicated_dp": 2 * (u - 1) / u * plan["dp_cut"] * row_bytes,
+            "replicated_flex": 2 * (n_nodes - 1) / n_nodes * flex_slot_rows * row_bytes if n_nodes > 1 else 0.0,
+        }
+        total = sum(per_gpu.values())
+        step_s = dev_ms / args.steps / 1e3
+        peer_peak = 770.0
+        nvlink = {"bytes_per_gpu_per_step": total, "breakdown": per_gpu,
+                  "achieved_gbs": round(total / step_s / 1e9, 1), "peak_gbs": peer_peak,
+                  "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
+                  "frac": round(total / step_s / 1e9 / peer_peak, 4),
+                  "bound_ms": round(total / (peer_peak * 1e9) * 1e3, 4)}
+
     cpu = None
     if dist.rank == 0 and u == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_port(batches[0], dest, plan, exp, B, D, args)
@@ -487,8 +520,10 @@ def run_ours(args, dist: Dist):
         "clocks": clk,
         "roofline": roofline,
         "a2a": a2a,
+        "nvlink": nvlink,
         "loss_last_step": loss,
         "step_trace_ms": trace,
+        **({"step_trace_ms_all_ranks": all_traces} if all_traces else {}),
         "wall_s_timed": round(wall, 4),
         "prep_wall_s": doc.get("prep_wall_s"),
     }

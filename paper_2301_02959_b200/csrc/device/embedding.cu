@@ -170,11 +170,21 @@ loss_finalize_kernel(const double* __restrict__ partials, unsigned count, double
 template <int VEC>
 __device__ __forceinline__ const float* grad_row(const GradSource& gs, uint32_t v, uint32_t dim) {
   if (v < gs.n_local) return gs.local + static_cast<uint64_t>(v) * dim;
-  const uint32_t r = v - gs.n_local;
-  if (gs.remote) return gs.remote + static_cast<uint64_t>(r) * dim;
-  int s = 0;  // source rank of received entry r (<= 8 ranges)
-  while (s + 1 < gs.npeer && r >= gs.src_start[s + 1]) ++s;
-  return gs.peer[s] + static_cast<uint64_t>(__ldg(gs.recv_pos + r)) * dim;
+  return gs.remote + static_cast<uint64_t>(v - gs.n_local) * dim;
+}
+
+// Where a dense-range row's reduced gradient goes (and its stamp, or null).
+template <int DIM>
+__device__ __forceinline__ float* dense_row(const DenseRange& d, uint32_t row, uint32_t** stamp) {
+  const uint32_t r = row - d.lo;
+  if (d.push_n) {
+    const uint32_t o = r / d.per;
+    const uint64_t slot = static_cast<uint64_t>(d.me) * d.per + (r - o * d.per);
+    *stamp = d.push_stamp[o] + slot;
+    return d.push_grad[o] + slot * DIM;
+  }
+  *stamp = d.stamp ? d.stamp + r : nullptr;
+  return d.grad + static_cast<uint64_t>(r) * DIM;
 }
 
 // Finishes one reduced row: dense-range rows park their gradient, others get
@@ -186,14 +196,11 @@ __device__ __forceinline__ void finish_row(uint32_t row, const float (&g)[DIM / 
                                            const DenseRange& d1) {
   constexpr int VEC = DIM / 32;
   const unsigned lane = threadIdx.x & 31u;
-  if (row >= d0.lo && row < d0.hi) {
-    store_lane<VEC>(d0.grad + static_cast<uint64_t>(row - d0.lo) * DIM + lane * VEC, g);
-    if (d0.stamp && lane == 0) d0.stamp[row - d0.lo] = d0.epoch;
-    return;
-  }
-  if (row >= d1.lo && row < d1.hi) {
-    store_lane<VEC>(d1.grad + static_cast<uint64_t>(row - d1.lo) * DIM + lane * VEC, g);
-    if (d1.stamp && lane == 0) d1.stamp[row - d1.lo] = d1.epoch;
+  if ((row >= d0.lo && row < d0.hi) || (row >= d1.lo && row < d1.hi)) {
+    const DenseRange& d = row < d0.hi && row >= d0.lo ? d0 : d1;
+    uint32_t* st = nullptr;
+    store_lane<VEC>(dense_row<DIM>(d, row, &st) + lane * VEC, g);
+    if (st && lane == 0) *st = d.epoch;
     return;
   }
   float* wp = weights + static_cast<uint64_t>(row) * DIM + lane * VEC;
@@ -299,14 +306,11 @@ __device__ __forceinline__ void group_finish_row(uint32_t row, const float (&g)[
   using Gp = Grouping<DIM>;
   constexpr int PER = Gp::PER, K = Gp::K, V = Gp::V;
   const uint64_t col = static_cast<uint64_t>(gl) * PER;
-  if (row >= d0.lo && row < d0.hi) {
-    store_vec<PER>(d0.grad + static_cast<uint64_t>(row - d0.lo) * DIM + col, g);
-    if (d0.stamp && gl == 0) d0.stamp[row - d0.lo] = d0.epoch;
-    return;
-  }
-  if (row >= d1.lo && row < d1.hi) {
-    store_vec<PER>(d1.grad + static_cast<uint64_t>(row - d1.lo) * DIM + col, g);
-    if (d1.stamp && gl == 0) d1.stamp[row - d1.lo] = d1.epoch;
+  if ((row >= d0.lo && row < d0.hi) || (row >= d1.lo && row < d1.hi)) {
+    const DenseRange& d = row < d0.hi && row >= d0.lo ? d0 : d1;
+    uint32_t* st = nullptr;
+    store_vec<PER>(dense_row<DIM>(d, row, &st) + col, g);
+    if (st && gl == 0) *st = d.epoch;
     return;
   }
   float* wp = weights + static_cast<uint64_t>(row) * DIM + col;
@@ -412,8 +416,9 @@ __device__ __forceinline__ void dense_store(uint32_t row, const float (&g)[Grp<D
                                             const DenseRange& d0, const DenseRange& d1) {
   constexpr int PER = Grp<DIM, G>::PER;
   const DenseRange& d = (row >= d0.lo && row < d0.hi) ? d0 : d1;
-  store_vec<PER>(d.grad + static_cast<uint64_t>(row - d.lo) * DIM + static_cast<uint64_t>(gl) * PER, g);
-  if (d.stamp && gl == 0) d.stamp[row - d.lo] = d.epoch;
+  uint32_t* st = nullptr;
+  store_vec<PER>(dense_row<DIM>(d, row, &st) + static_cast<uint64_t>(gl) * PER, g);
+  if (st && gl == 0) *st = d.epoch;
 }
 
 // acc += rows vals[k..e) (left to right), two rows in flight.
@@ -502,6 +507,7 @@ seg_pair_kernel(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ 
       else dense_store<DIM, G>(kb, acc_b, gl, d0, d1);
     }
   }
+  if (d0.push_n | d1.push_n) __threadfence_system();  // partials stored to peers
 }
 
 template <int DIM>
@@ -549,6 +555,7 @@ seg_short_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__
     }
     group_finish_row<DIM>(row, acc, gl, gmask, weights, state, opt, d0, d1);
   }
+  if (d0.push_n | d1.push_n) __threadfence_system();  // partials stored to peers
 }
 
 // piece_off[i] = exclusive prefix of pieces over the long list.
@@ -638,6 +645,7 @@ long_combine_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restric
     }
     finish_row<DIM>(keys[starts[j]], acc, weights, state, opt, d0, d1);
   }
+  if (d0.push_n | d1.push_n) __threadfence_system();  // partials stored to peers
 }
 
 template <int DIM>
@@ -660,97 +668,38 @@ template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 replica_update_kernel(ReplicaGroup grp, OptParams opt) {
   constexpr int VEC = DIM / 32;
-  constexpr int R = DIM <= 128 ? 4 : 1;  // rows in flight per warp (peer latency)
   const unsigned lane = threadIdx.x & 31u;
-  const uint32_t per = (grp.rows + grp.size - 1) / grp.size;
-  const uint32_t lo = per * grp.me;
-  const uint32_t hi = min(grp.rows, lo + per);
+  const uint32_t lo = grp.per * grp.me;
+  const uint32_t n = lo < grp.rows ? min(grp.per, grp.rows - lo) : 0u;  // rows I own
   const uint32_t gwarp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
   float* mine = grp.weights[grp.me];
   float* my_state = grp.state[grp.me];
-  for (uint32_t r0 = lo + gwarp * R; r0 < hi; r0 += nwarps * R) {
-    float g[R][VEC];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      if (r0 + i >= hi) continue;
-      const uint64_t off = static_cast<uint64_t>(r0 + i) * DIM + lane * VEC;
-      float part[kMaxGradPeers][VEC];
-#pragma unroll
-      for (int k = 0; k < kMaxGradPeers; ++k) {  // all members' loads in flight
-        if (k < grp.size) load_lane<VEC>(grp.grads[k] + off, part[k]);
-      }
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) g[i][j] = part[0][j];
-#pragma unroll
-      for (int k = 1; k < kMaxGradPeers; ++k) {
-        if (k < grp.size) {
-#pragma unroll
-          for (int j = 0; j < VEC; ++j) g[i][j] = __fadd_rn(g[i][j], part[k][j]);
-        }
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const uint32_t r = r0 + i;
-      if (r >= hi) continue;
-      // optimizer on my replica, then broadcast the row (+ state) to the others
-      finish_row<DIM>(r, g[i], mine, my_state, opt, DenseRange{}, DenseRange{});
-      __syncwarp();
-      const uint64_t off = static_cast<uint64_t>(r) * DIM + lane * VEC;
-      float w[VEC];
-      load_lane<VEC>(mine + off, w);
-      const float st = my_state ? my_state[r] : 0.0f;
+  for (uint32_t base = gwarp * 32; base < n; base += nwarps * 32) {
+    // 32 rows' stamps at once (coalesced), then the rows some member touched
+    const uint32_t i = base + lane;
+    uint32_t members = 0;
+    if (i < n) {
 #pragma unroll
       for (int k = 0; k < kMaxGradPeers; ++k) {
-        if (k < grp.size && k != grp.me) {
-          store_lane<VEC>(grp.weights[k] + off, w);
-          if (my_state && lane == 0) grp.state[k][r] = st;
+        if (k < grp.size && __ldg(grp.recv_stamp + static_cast<uint64_t>(k) * grp.per + i) == grp.epoch) {
+          members |= 1u << k;
         }
       }
-    }
-  }
-  __threadfence_system();
-}
-
-// Stamped variant: a warp tests 32 rows' stamps at once (one 4-byte peer
-// load per member per row), then walks the rows some member touched.
-template <int DIM>
-__global__ void __launch_bounds__(kThreads)
-replica_sparse_kernel(ReplicaGroup grp, OptParams opt) {
-  constexpr int VEC = DIM / 32;
-  const unsigned lane = threadIdx.x & 31u;
-  const uint32_t per = (grp.rows + grp.size - 1) / grp.size;
-  const uint32_t lo = per * grp.me;
-  const uint32_t hi = min(grp.rows, lo + per);
-  const uint32_t gwarp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
-  float* mine = grp.weights[grp.me];
-  float* my_state = grp.state[grp.me];
-  for (uint32_t base = lo + gwarp * 32; base < hi; base += nwarps * 32) {
-    const uint32_t r = base + lane;
-    uint32_t members = 0;
-    if (r < hi) {
-      uint32_t st[kMaxGradPeers];
-#pragma unroll
-      for (int k = 0; k < kMaxGradPeers; ++k) st[k] = k < grp.size ? grp.stamps[k][r] : 0u;
-#pragma unroll
-      for (int k = 0; k < kMaxGradPeers; ++k) members |= (k < grp.size && st[k] == grp.epoch) ? 1u << k : 0u;
     }
     unsigned active = __ballot_sync(0xFFFFFFFFu, members != 0);
     while (active) {
       const int b = __ffs(active) - 1;
       active &= active - 1;
-      const uint32_t row = base + b;
       const uint32_t m = __shfl_sync(0xFFFFFFFFu, members, b);
-      const uint64_t off = static_cast<uint64_t>(row) * DIM + lane * VEC;
+      const uint32_t row = lo + base + b;
       float part[kMaxGradPeers][VEC];
 #pragma unroll
-      for (int k = 0; k < kMaxGradPeers; ++k) {  // touched members' loads in flight
-        if ((m >> k) & 1u) load_lane<VEC>(grp.grads[k] + off, part[k]);
+      for (int k = 0; k < kMaxGradPeers; ++k) {  // touched members' partials in flight
+        if ((m >> k) & 1u) {
+          load_lane<VEC>(grp.recv + (static_cast<uint64_t>(k) * grp.per + base + b) * DIM + lane * VEC, part[k]);
+        }
       }
-      // group-rank order over the members that touched the row (an untouched
-      // member's partial is zero: adding it changes nothing)
       float g[VEC];
       bool first = true;
 #pragma unroll
@@ -763,6 +712,7 @@ replica_sparse_kernel(ReplicaGroup grp, OptParams opt) {
       }
       finish_row<DIM>(row, g, mine, my_state, opt, DenseRange{}, DenseRange{});
       __syncwarp();
+      const uint64_t off = static_cast<uint64_t>(row) * DIM + lane * VEC;
       float w[VEC];
       load_lane<VEC>(mine + off, w);
       const float st = my_state ? my_state[row] : 0.0f;
@@ -972,18 +922,11 @@ void launch_dense_update(const float* grad, uint32_t rows, uint32_t row_lo, uint
 void launch_replica_update(const ReplicaGroup& grp, uint32_t dim, const OptParams& opt,
                            cudaStream_t stream) {
   if (grp.rows == 0 || grp.size == 0) return;
-  const uint32_t per = (grp.rows + grp.size - 1) / grp.size;
   const unsigned grid = std::max<unsigned>(
-      1, std::min<unsigned>(persistent_grid(g_compute_blocks_per_sm), ceil_div(per, kThreads / 32)));
+      1, std::min<unsigned>(persistent_grid(g_compute_blocks_per_sm), ceil_div(grp.per, kThreads)));
   dispatch_dim(dim, [&](auto D) {
     constexpr int DIM = decltype(D)::value;
-    if (grp.stamps[0]) {
-      const unsigned sgrid = std::max<unsigned>(
-          1, std::min<unsigned>(persistent_grid(g_compute_blocks_per_sm), ceil_div(per, kThreads)));
-      replica_sparse_kernel<DIM><<<sgrid, kThreads, 0, stream>>>(grp, opt);
-    } else {
-      replica_update_kernel<DIM><<<grid, kThreads, 0, stream>>>(grp, opt);
-    }
+    replica_update_kernel<DIM><<<grid, kThreads, 0, stream>>>(grp, opt);
   });
   TSD_LAUNCH_CHECK();
 }

@@ -34,28 +34,30 @@ struct OptParams {
 // With `stamp`, the row's stamp[row - dense_lo] is set to `epoch` as well:
 // the replica update then reads only rows stamped this step, so the dense
 // buffer never needs clearing and untouched rows cost no NVLink traffic.
+constexpr int kMaxGradPeers = 8;
+
+// Push mode (U > 1 over peer memory): the range is the replicated rows of a
+// replica group of push_n members; relative row r belongs to member
+// o = r / per, which receives every member's partial in its [push_n][per]
+// buffer: the row's gradient is STORED (NVLink) to push_grad[o] at slot
+// me * per + r % per, and its stamp to push_stamp[o] at the same slot.
 struct DenseRange {
   uint32_t lo = 0, hi = 0;
   float* grad = nullptr;
   uint32_t* stamp = nullptr;
   uint32_t epoch = 0;
+  uint32_t push_n = 0, per = 0, me = 0;
+  float* push_grad[kMaxGradPeers] = {};
+  uint32_t* push_stamp[kMaxGradPeers] = {};
 };
 
-constexpr int kMaxGradPeers = 8;
-
 // Gradient source of sorted entry value v: v < n_local -> local grads
-// [n_local x dim]; else r = v - n_local is a received entry: staged mode
-// reads remote[r x dim]; peer mode (remote == nullptr) reads the row straight
-// from the requesting rank's gradient buffer over NVLink:
-// peer[s][recv_pos[r] x dim] with s the source whose recv range holds r.
+// [n_local x dim]; else r = v - n_local is a received entry, remote[r x dim]
+// (received rows staged in local HBM by the exchange).
 struct GradSource {
   const float* local = nullptr;
   const float* remote = nullptr;
   uint32_t n_local = 0;
-  const uint32_t* recv_pos = nullptr;
-  const float* peer[kMaxGradPeers] = {};
-  uint32_t src_start[kMaxGradPeers + 1] = {};
-  int npeer = 0;
 };
 
 // out[i] = W[local(rows[i])] for every occurrence served locally; remote
@@ -112,25 +114,28 @@ void launch_dense_update(const float* grad, uint32_t rows, uint32_t row_lo, uint
                          float* weights, float* state, const OptParams& opt, cudaStream_t stream);
 
 // Replicated-tier update over peer memory (replaces all-reduce + dense
-// update): the `size` ranks of a replica group each own a contiguous slice of
-// the group's dense rows; for each owned row the owner sums the members'
-// partial gradients grads[0..size) IN GROUP-RANK ORDER (peer loads), applies
-// the optimizer to its replica and stores the updated row (and Adagrad state)
-// into every member's replica (peer stores).  Deterministic and identical on
-// all replicas by construction.  With stamps, a member's partial counts only
-// where its stamp equals `epoch` (rows it touched this step); rows no member
-// touched have a zero gradient, which leaves SGD and row-wise Adagrad rows
-// unchanged, so they are skipped without a read.
+// update): member `me` of a replica group owns the group's rows
+// [me * per, (me + 1) * per).  Every member has already pushed its partial
+// gradient of those rows into the owner's local receive buffer
+// recv[size][per][dim] (slot k = member k; DenseRange push mode), stamped
+// with `epoch` where it touched the row.  The owner sums the stamped
+// partials IN GROUP-RANK ORDER (an untouched member's partial is zero:
+// skipping it changes nothing), applies the optimizer to its replica and
+// stores the updated row (and Adagrad state) into every member's replica
+// (peer stores).  Rows no member touched have a zero gradient, which leaves
+// SGD and row-wise Adagrad rows unchanged, so they are skipped.  All loads
+// are local; deterministic and identical on all replicas by construction.
 struct ReplicaGroup {
   int size = 0;
-  int me = 0;                              // my index in the group
-  const float* grads[kMaxGradPeers] = {};  // dense partials [rows x dim], by group rank
-  const uint32_t* stamps[kMaxGradPeers] = {};  // per-row epoch stamps (all or none)
+  int me = 0;                          // my index in the group
+  const float* recv = nullptr;         // [size][per][dim], local
+  const uint32_t* recv_stamp = nullptr;  // [size][per], local
   uint32_t epoch = 0;
-  float* weights[kMaxGradPeers] = {};      // replicas: weights + row_lo * dim
-  float* state[kMaxGradPeers] = {};        // Adagrad state + row_lo (may be null)
-  uint32_t rows = 0;                       // dense rows of the tier
-  uint32_t row_lo = 0;                     // local id of dense row 0
+  uint32_t per = 0;                    // rows owned per member
+  float* weights[kMaxGradPeers] = {};  // replicas: weights + row_lo * dim
+  float* state[kMaxGradPeers] = {};    // Adagrad state + row_lo (may be null)
+  uint32_t rows = 0;                   // replicated rows of the tier
+  uint32_t row_lo = 0;                 // local id of replicated row 0
 };
 
 void launch_replica_update(const ReplicaGroup& grp, uint32_t dim, const OptParams& opt,

@@ -4,6 +4,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -150,6 +151,69 @@ void launch_pull_grads(const PullGrads& pg, const uint32_t* recv_pos, uint64_t c
     case 2: pull_grads_kernel<2><<<grid, kThreads, 0, stream>>>(pg, recv_pos, count, dst, dim); break;
     case 4: pull_grads_kernel<4><<<grid, kThreads, 0, stream>>>(pg, recv_pos, count, dst, dim); break;
     default: pull_grads_kernel<8><<<grid, kThreads, 0, stream>>>(pg, recv_pos, count, dst, dim); break;
+  }
+  TSD_LAUNCH_CHECK();
+}
+
+template <int VEC4>
+__global__ void __launch_bounds__(kThreads)
+push_grads_kernel(PushTable t, const uint32_t* __restrict__ order, const float* __restrict__ grad,
+                  uint32_t dim) {
+  constexpr int kRows = 4;  // local loads in flight per warp
+  const unsigned lane = threadIdx.x & 31u;
+  const uint64_t gwarp = (static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * kThreads) >> 5;
+  const uint64_t total = t.run_start[t.n];
+  const uint32_t vecs = dim / 4;
+  for (uint64_t r0 = gwarp * kRows; r0 < total; r0 += nwarps * kRows) {
+    float4 v[kRows][VEC4];
+    float4* dst[kRows];
+#pragma unroll
+    for (int k = 0; k < kRows; ++k) {
+      const uint64_t r = r0 + k;
+      dst[k] = nullptr;
+      if (r >= total) continue;
+      int s = 0;
+      while (s + 1 < t.n && r >= t.run_start[s + 1]) ++s;
+      const uint64_t j = r - t.run_start[s];
+      const float4* src = reinterpret_cast<const float4*>(
+          grad + static_cast<uint64_t>(__ldg(order + t.run[s].src_begin + j)) * dim);
+      dst[k] = reinterpret_cast<float4*>(t.run[s].dst + j * dim);
+#pragma unroll
+      for (int q = 0; q < VEC4; ++q) {
+        const uint32_t c = lane + 32u * q;
+        if (c < vecs) v[k][q] = __ldg(src + c);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kRows; ++k) {
+      if (!dst[k]) continue;
+#pragma unroll
+      for (int q = 0; q < VEC4; ++q) {
+        const uint32_t c = lane + 32u * q;
+        if (c < vecs) dst[k][c] = v[k][q];  // NVLink store into the server's receive buffer
+      }
+    }
+  }
+  __threadfence_system();
+}
+
+void launch_push_grads(const PushTable& t, const uint32_t* order, const float* grad, uint32_t dim,
+                       cudaStream_t stream) {
+  if (t.n == 0 || t.run_start[t.n] == 0) return;
+  // one block per SM saturates NVLink stores (~700 GB/s) and leaves the rest
+  // of every SM to the sort it overlaps (TIERSHARD_PUSH_BLOCKS = per SM)
+  static const unsigned per_sm = [] {
+    const char* e = std::getenv("TIERSHARD_PUSH_BLOCKS");
+    return e ? static_cast<unsigned>(std::max(1, std::atoi(e))) : 1u;
+  }();
+  const unsigned grid = per_sm * sm_count();
+  const uint32_t vec4 = (dim / 4 + 31) / 32;
+  switch (vec4) {
+    case 1: push_grads_kernel<1><<<grid, kThreads, 0, stream>>>(t, order, grad, dim); break;
+    case 2: push_grads_kernel<2><<<grid, kThreads, 0, stream>>>(t, order, grad, dim); break;
+    case 4: push_grads_kernel<4><<<grid, kThreads, 0, stream>>>(t, order, grad, dim); break;
+    default: push_grads_kernel<8><<<grid, kThreads, 0, stream>>>(t, order, grad, dim); break;
   }
   TSD_LAUNCH_CHECK();
 }

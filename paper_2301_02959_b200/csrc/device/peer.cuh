@@ -102,6 +102,25 @@ struct PullGrads {
 void launch_pull_grads(const PullGrads& pg, const uint32_t* recv_pos, uint64_t count, float* dst,
                        uint32_t dim, cudaStream_t stream);
 
+// Push: the requester STORES the gradient rows of its remote occurrences
+// into the servers' receive buffers (NVLink stores, fire-and-forget; peer
+// stores sustain ~700 GB/s with one block per SM where peer loads need four).
+// Run k moves `count` rows: row j comes from grad[order[src_begin + j]] and
+// lands at dst + j * dim (dst = the server's receive buffer at this
+// requester's slot).
+struct PushRun {
+  uint64_t src_begin;
+  uint64_t count;
+  float* dst;
+};
+struct PushTable {
+  PushRun run[2 * kMaxPeerRanks];
+  uint64_t run_start[2 * kMaxPeerRanks + 1];
+  int n;
+};
+void launch_push_grads(const PushTable& t, const uint32_t* order, const float* grad, uint32_t dim,
+                       cudaStream_t stream);
+
 void launch_serve_rows(const float* weights, const uint32_t* recv_ids, const uint32_t* recv_pos,
                        const ServeTable& st, uint32_t dim, cudaStream_t stream);
 

@@ -89,13 +89,14 @@ enum Phase : int {
   kPhaseDenseUpdate,
   kPhaseReplicaUpdate,
   kPhaseSegmentLong,
+  kPhaseRendezvous,
   kNumPhases
 };
 
 const char* const kPhaseNames[kNumPhases] = {
     "route",         "gather",         "exchange_fwd", "scatter",  "exchange_bwd",
     "dedup_sort",    "segment_starts", "segment_update", "allreduce", "dense_update",
-    "replica_update", "segment_long"};
+    "replica_update", "segment_long", "rendezvous"};
 
 }  // namespace
 }  // namespace tsd
@@ -155,21 +156,21 @@ struct ts_table {
   std::vector<const uint32_t*> peer_ids, peer_pos;  // peers' request lists (mapped)
   std::vector<double*> peer_loss;                   // peers' remote-loss slots (mapped)
   std::vector<const float*> peer_grad;              // peers' gradient buffers (mapped)
-  std::vector<const float*> peer_dense_dp, peer_dense_flex;  // peers' dense partials (mapped)
-  std::vector<const uint32_t*> peer_stamp_dp, peer_stamp_flex;  // and their row stamps
+  std::vector<float*> peer_dense_dp, peer_dense_flex;  // peers' partial receive buffers (mapped)
+  std::vector<uint32_t*> peer_stamp_dp, peer_stamp_flex;  // and their slot stamps
+  uint32_t per_dp = 0, per_flex = 0;  // replicated rows owned per group member
   std::vector<float*> peer_w, peer_state;           // peers' shards (mapped)
   tsd::IpcExport my_export{};                       // staging for the step payload
   uint64_t remote_loss_slots = 0;                   // U * kServeGrid
   // schedule knobs (env, read at creation; defaults = fastest measured):
   //   TIERSHARD_REPLICA=serial|concurrent  replica update after the DP
   //     segments on the compute stream, or on the comm stream beside the RW
-  //     segments;  TIERSHARD_PULL_GRADS=1|0  stage remote gradient rows into
-  //     HBM with one NVLink gather, or load them from peer memory in-kernel.
-  //     Staging is the default: equal on device-resident steps, and the
-  //     in-kernel peer loads measured 8x slower on the host-buffer entry
-  //     point (ts_table_train_step_host, 4.2 ms vs 0.5 ms at U = 2)
+  //     segments;  TIERSHARD_GRADS=push|pull  remote gradient rows reach
+  //     their server by requester-side NVLink stores (push) or a
+  //     server-side NVLink gather (pull).
   bool replica_concurrent = true;
-  bool pull_grads = true;
+  bool grads_push = true;
+  bool push_first = false;
 
   size_t step_payload_bytes() const { return ((nb() + 1) * 4 + 7) / 8 * 8 + sizeof(tsd::IpcExport); }
   std::vector<uint8_t> allgather_bytes(const void* mine, size_t bytes);
@@ -384,14 +385,21 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     order.ensure(c.max_occurrences);
     send_ids.ensure(c.max_occurrences);
     send_rows.ensure(c.max_occurrences * c.dim);
+    // received gradient rows: peers store into this buffer (P2P push), so it
+    // never moves -- sized once for the worst case, every peer's whole batch
+    recv_rows.ensure(uint64_t{U - 1} * c.max_occurrences * c.dim);
     bucket_start.ensure(nb() + 2);
     all_counts.ensure(static_cast<uint64_t>(U) * (nb() + 1));
-    dense_dp.ensure(std::max<uint64_t>(dp_rows, 1) * c.dim);
-    if (N > 1) dense_flex.ensure(std::max<uint64_t>(flex_rows, 1) * c.dim);
-    stamp_dp.ensure(std::max<uint64_t>(dp_rows, 1));
+    // replicated-row gradients: [U][per_dp][D] receive slots (P2P push
+    // mode; the staged path uses the first dp_rows x D as a dense buffer)
+    per_dp = static_cast<uint32_t>((dp_rows + U - 1) / U);
+    dense_dp.ensure(std::max<uint64_t>(uint64_t{U} * per_dp, 1) * c.dim);
+    stamp_dp.ensure(std::max<uint64_t>(uint64_t{U} * per_dp, 1));
     TSD_CUDA(cudaMemsetAsync(stamp_dp.ptr, 0, sizeof(uint32_t) * stamp_dp.cap, stream));
     if (N > 1) {
-      stamp_flex.ensure(std::max<uint64_t>(flex_rows, 1));
+      per_flex = static_cast<uint32_t>((flex_rows + N - 1) / N);
+      dense_flex.ensure(std::max<uint64_t>(uint64_t{N} * per_flex, 1) * c.dim);
+      stamp_flex.ensure(std::max<uint64_t>(uint64_t{N} * per_flex, 1));
       TSD_CUDA(cudaMemsetAsync(stamp_flex.ptr, 0, sizeof(uint32_t) * stamp_flex.cap, stream));
     }
     TSD_CUDA(cudaStreamSynchronize(stream));
@@ -469,7 +477,8 @@ void ts_table::setup_p2p() {
   p2p = ok != 0;
   if (!p2p) return;
   if (const char* env = std::getenv("TIERSHARD_REPLICA")) replica_concurrent = std::string(env) != "serial";
-  if (const char* env = std::getenv("TIERSHARD_PULL_GRADS")) pull_grads = std::string(env) != "0";
+  if (const char* env = std::getenv("TIERSHARD_GRADS")) grads_push = std::string(env) != "pull";
+  if (const char* env = std::getenv("TIERSHARD_PUSH_ORDER")) push_first = std::string(env) == "first";
   // export the table-owned buffers peers read or write
   auto exp_or_none = [](const void* p) {
     IpcExport e;
@@ -504,12 +513,12 @@ void ts_table::setup_p2p() {
     peer_ids[p] = static_cast<const uint32_t*>(peers.open(pp, e[0]));
     peer_pos[p] = static_cast<const uint32_t*>(peers.open(pp, e[1]));
     peer_loss[p] = static_cast<double*>(peers.open(pp, e[2]));
-    peer_dense_dp[p] = static_cast<const float*>(open_opt(e[3]));
+    peer_dense_dp[p] = static_cast<float*>(open_opt(e[3]));
     peer_w[p] = static_cast<float*>(peers.open(pp, e[4]));
     peer_state[p] = static_cast<float*>(open_opt(e[5]));
-    peer_dense_flex[p] = static_cast<const float*>(open_opt(e[6]));
-    peer_stamp_dp[p] = static_cast<const uint32_t*>(open_opt(e[7]));
-    peer_stamp_flex[p] = static_cast<const uint32_t*>(open_opt(e[8]));
+    peer_dense_flex[p] = static_cast<float*>(open_opt(e[6]));
+    peer_stamp_dp[p] = static_cast<uint32_t*>(open_opt(e[7]));
+    peer_stamp_flex[p] = static_cast<uint32_t*>(open_opt(e[8]));
   }
   peer_grad.assign(U, nullptr);
   xfer.ensure(step_payload_bytes() * U);
@@ -922,13 +931,92 @@ void ts_table::backward_p2p(const float* d_grad) {
   TSD_CUDA(cudaEventRecord(ev_bwd0, stream));  // our gradient is complete here
   launch_build_entries(last_rows, order.ptr + n_remote, n_local_occ, rv, recv_ids.ptr, recv_before,
                        recv_total, static_cast<uint32_t>(occ), entry_keys.ptr, entry_vals.ptr, stream);
-  // dense partials are stamped with the step's epoch instead of cleared
+  // replicated rows' partials are pushed to their owners' receive slots and
+  // stamped with the step's epoch (no clears; untouched slots are ignored)
   if (++epoch == 0) epoch = 1;  // (2^32 steps) 0 is the initial stamp
-  if (dp_rows) d0 = DenseRange{0, static_cast<uint32_t>(dp_rows), dense_dp.ptr, stamp_dp.ptr, epoch};
-  if (N > 1 && flex_rows) {
-    d1 = DenseRange{static_cast<uint32_t>(dp_rows), static_cast<uint32_t>(dp_rows + flex_rows),
-                    dense_flex.ptr, stamp_flex.ptr, epoch};
+  if (dp_rows) {
+    d0.lo = 0;
+    d0.hi = static_cast<uint32_t>(dp_rows);
+    d0.epoch = epoch;
+    d0.push_n = U;
+    d0.per = per_dp;
+    d0.me = g;
+    for (uint32_t p = 0; p < U; ++p) {
+      d0.push_grad[p] = peer_dense_dp[p];
+      d0.push_stamp[p] = peer_stamp_dp[p];
+    }
   }
+  if (N > 1 && flex_rows) {  // group: the same slot in every node, node order
+    d1.lo = static_cast<uint32_t>(dp_rows);
+    d1.hi = static_cast<uint32_t>(dp_rows + flex_rows);
+    d1.epoch = epoch;
+    d1.push_n = N;
+    d1.per = per_flex;
+    d1.me = node;
+    for (uint32_t k = 0; k < N; ++k) {
+      d1.push_grad[k] = peer_dense_flex[k * W + slot];
+      d1.push_stamp[k] = peer_stamp_flex[k * W + slot];
+    }
+  }
+  // ---- remote gradient rows -> their servers -------------------------------
+  // push (default): after one all-gather of the servers' receive buffers
+  // (the rendezvous after which every rank's gradient is complete), each
+  // rank STORES the gradients of its remote occurrences into its servers'
+  // receive slots (the order the servers pulled our request lists in), then
+  // a barrier; pull (TIERSHARD_GRADS=pull): each server gathers them from
+  // the requesters' gradient buffers with peer loads.  Either way the remote
+  // rows end up in local HBM, recv_rows[r] for received entry r.  The
+  // transfer kernel runs on `xs`: the comm stream (overlapping the sort) or,
+  // with TIERSHARD_PUSH_ORDER=first, the compute stream ahead of the sort.
+  const auto exchange_grads = [&](cudaStream_t xs) {
+    TSD_CUDA(cudaStreamWaitEvent(comm, ev_bwd0, 0));
+    int tx = phase_begin(kPhaseExchangeBwd, xs);
+    if (recv_total * cfg.dim > recv_rows.cap) fail(TS_ERR_INTERNAL, "table: receive buffer overflow");
+    const IpcExport mine = export_pointer(grads_push ? static_cast<const void*>(recv_rows.ptr) : d_grad);
+    const std::vector<uint8_t> all = allgather_bytes(&mine, sizeof(mine));
+    if (grads_push) {
+      PushTable pt{};
+      for (uint32_t p = 0; p < U; ++p) {
+        if (p == g) continue;
+        IpcExport e;
+        std::memcpy(&e, all.data() + sizeof(e) * p, sizeof(e));
+        float* server_recv = static_cast<float*>(peers.open(static_cast<int>(p), e));
+        ExchangePlan sp;  // server p's receive layout: which slots hold our entries
+        exchange_plan(N, W, p, h_counts.data(), &sp);
+        for (int part = 0; part < 2; ++part) {
+          const uint64_t cnt = send_cnt[2 * p + part];
+          if (!cnt) continue;
+          pt.run_start[pt.n] = pt.n ? pt.run_start[pt.n - 1] + pt.run[pt.n - 1].count : 0;
+          pt.run[pt.n++] = PushRun{send_off[2 * p + part], cnt, server_recv + sp.recv_off[2 * g + part] * cfg.dim};
+        }
+      }
+      pt.run_start[pt.n] = pt.n ? pt.run_start[pt.n - 1] + pt.run[pt.n - 1].count : 0;
+      launch_push_grads(pt, order.ptr, d_grad, cfg.dim, xs);
+      if (xs != comm) {
+        TSD_CUDA(cudaEventRecord(ev_dense, xs));
+        TSD_CUDA(cudaStreamWaitEvent(comm, ev_dense, 0));
+      }
+      barrier_on_comm();  // every requester's rows have landed in every server
+    } else {
+      PullGrads pg{};
+      for (uint32_t p = 0; p < U; ++p) {
+        if (p == g) continue;
+        IpcExport e;
+        std::memcpy(&e, all.data() + sizeof(e) * p, sizeof(e));
+        pg.src_start[pg.nsrc] = static_cast<uint32_t>(recv_off[2 * p]);
+        pg.src[pg.nsrc++] = static_cast<const float*>(peers.open(static_cast<int>(p), e));
+      }
+      pg.src_start[pg.nsrc] = static_cast<uint32_t>(recv_total);
+      launch_pull_grads(pg, recv_pos.ptr, recv_total, recv_rows.ptr, cfg.dim, xs);
+      if (xs != comm) {
+        TSD_CUDA(cudaEventRecord(ev_dense, xs));
+        TSD_CUDA(cudaStreamWaitEvent(comm, ev_dense, 0));
+      }
+    }
+    phase_end(tx);
+    TSD_CUDA(cudaEventRecord(ev_grads, comm));
+  };
+  if (push_first) exchange_grads(stream);
   int t = phase_begin(kPhaseSort);
   radix_sort_pairs(entry_keys.ptr, entry_vals.ptr, m, bits_for(local_rows ? local_rows - 1 : 0), rb, &sk, &sv,
                    stream);
@@ -939,44 +1027,17 @@ void ts_table::backward_p2p(const float* d_grad) {
   launch_segment_split(sk, starts.ptr, nseg.ptr, dense_hi, seg_split.ptr, stream);
   phase_end(t);
 
-  // ---- comm stream: gradient-buffer exports (rendezvous: all grads ready) --
-  TSD_CUDA(cudaStreamWaitEvent(comm, ev_bwd0, 0));
-  t = phase_begin(kPhaseExchangeBwd, comm);
-  const IpcExport mine = export_pointer(d_grad);
-  const std::vector<uint8_t> all = allgather_bytes(&mine, sizeof(mine));
-  phase_end(t);
-  // Remote gradient rows: one NVLink-bandwidth-bound gather straight out of
-  // the requesters' gradient buffers into local HBM (overlaps the sort); the
-  // segment kernels then stay on local memory.
-  PullGrads pg{};
-  for (uint32_t p = 0; p < U; ++p) {
-    if (p == g) continue;
-    IpcExport e;
-    std::memcpy(&e, all.data() + sizeof(e) * p, sizeof(e));
-    pg.src_start[pg.nsrc] = static_cast<uint32_t>(recv_off[2 * p]);
-    pg.src[pg.nsrc++] = static_cast<const float*>(peers.open(static_cast<int>(p), e));
-  }
-  pg.src_start[pg.nsrc] = static_cast<uint32_t>(recv_total);
+  if (!push_first) exchange_grads(comm);
   GradSource gs;
   gs.local = d_grad;
   gs.n_local = static_cast<uint32_t>(occ);
-  if (pull_grads) {
-    recv_rows.ensure(std::max<uint64_t>(recv_total, 1) * cfg.dim);
-    launch_pull_grads(pg, recv_pos.ptr, recv_total, recv_rows.ptr, cfg.dim, comm);
-    gs.remote = recv_rows.ptr;
-  } else {  // segment kernels load remote rows from peer memory directly
-    gs.recv_pos = recv_pos.ptr;
-    gs.npeer = pg.nsrc;
-    for (int k = 0; k < pg.nsrc; ++k) {
-      gs.peer[k] = pg.src[k];
-      gs.src_start[k] = pg.src_start[k];
-    }
-    gs.src_start[pg.nsrc] = pg.src_start[pg.nsrc];
-  }
-  TSD_CUDA(cudaEventRecord(ev_grads, comm));
-  TSD_CUDA(cudaStreamWaitEvent(stream, ev_grads, 0));
+  gs.remote = recv_rows.ptr;
 
-  // ---- replicated rows first; their all-reduce overlaps the RW updates ----
+  // ---- replicated rows first; their reduction overlaps the RW updates.  With
+  // one node the replicated (DP) segments hold local entries only and start
+  // without the remote rows; Flex rows replicated across nodes need them.
+  const bool dense_needs_remote = N > 1 && flex_rows;
+  if (dense_needs_remote) TSD_CUDA(cudaStreamWaitEvent(stream, ev_grads, 0));
   t = phase_begin(kPhaseSegmentUpdate);
   launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr, seg_split.ptr + 1, m, cfg.dim, gs, d_w, d_state,
                         opt, d0, d1, sc, stream);
@@ -984,33 +1045,35 @@ void ts_table::backward_p2p(const float* d_grad) {
   t = phase_begin(kPhaseSegmentLong);
   launch_segment_long(sk, sv, starts.ptr, m, cfg.dim, gs, d_w, d_state, opt, d0, d1, sc, stream);
   phase_end(t);
+  if (!dense_needs_remote) TSD_CUDA(cudaStreamWaitEvent(stream, ev_grads, 0));
   // ---- replicated tiers over peer memory: after a rendezvous (all ranks'
   // partials written), each rank reduces its slice of the replicated rows in
   // group-rank order, updates it and broadcasts it to every replica --------
   TSD_CUDA(cudaEventRecord(ev_dense, stream));
   TSD_CUDA(cudaStreamWaitEvent(comm, ev_dense, 0));
   cudaStream_t rs = replica_concurrent ? comm : stream;
-  t = phase_begin(kPhaseReplicaUpdate, comm);
+  t = phase_begin(kPhaseRendezvous, comm);
   barrier_on_comm();
+  phase_end(t);
   if (!replica_concurrent) {
-    phase_end(t);
     TSD_CUDA(cudaEventRecord(ev_ar, comm));
     TSD_CUDA(cudaStreamWaitEvent(stream, ev_ar, 0));
-    t = phase_begin(kPhaseReplicaUpdate, stream);
   }
+  t = phase_begin(kPhaseReplicaUpdate, rs);
   if (dp_rows) {
     ReplicaGroup grp;
     grp.size = static_cast<int>(U);
     grp.me = static_cast<int>(g);
     grp.rows = static_cast<uint32_t>(dp_rows);
     grp.row_lo = 0;
+    grp.recv = dense_dp.ptr;
+    grp.recv_stamp = stamp_dp.ptr;
+    grp.per = per_dp;
+    grp.epoch = epoch;
     for (uint32_t p = 0; p < U; ++p) {
-      grp.grads[p] = peer_dense_dp[p];
-      grp.stamps[p] = peer_stamp_dp[p];
       grp.weights[p] = peer_w[p];
       grp.state[p] = peer_state[p];
     }
-    grp.epoch = epoch;
     launch_replica_update(grp, cfg.dim, opt, rs);
   }
   if (N > 1 && flex_rows) {
@@ -1021,11 +1084,12 @@ void ts_table::backward_p2p(const float* d_grad) {
     grp.row_lo = static_cast<uint32_t>(dp_rows);
     for (uint32_t k = 0; k < N; ++k) {
       const uint32_t p = k * W + slot;
-      grp.grads[k] = peer_dense_flex[p];
-      grp.stamps[k] = peer_stamp_flex[p];
       grp.weights[k] = peer_w[p] + dp_rows * cfg.dim;
       grp.state[k] = peer_state[p] ? peer_state[p] + dp_rows : nullptr;
     }
+    grp.recv = dense_flex.ptr;
+    grp.recv_stamp = stamp_flex.ptr;
+    grp.per = per_flex;
     grp.epoch = epoch;
     launch_replica_update(grp, cfg.dim, opt, rs);
   }

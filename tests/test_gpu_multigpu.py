@@ -48,15 +48,15 @@ def free_port():
 
 
 CASES = [(1, 2, 1, "p2p"), (2, 1, 1, "p2p"), (2, 1, 0, "p2p"), (2, 2, 1, "p2p"), (1, 4, 1, "p2p"),
-         (1, 2, 1, "p2p_peerload"), (2, 2, 1, "p2p_peerload"),
+         (1, 2, 1, "p2p_pull"), (2, 2, 1, "p2p_pull"), (1, 4, 0, "p2p_pull"),
          (1, 2, 1, "nccl"), (2, 2, 1, "nccl"), (2, 1, 0, "nccl")]
 
 
 @pytest.mark.parametrize("n_nodes,w,opt,exchange", CASES)
 def test_multi_gpu_matches_oracle(cuda, tmp_path, n_nodes, w, opt, exchange):
-    """exchange: "p2p" = peer-memory serve + staged gradient pull (default on
-    one node), "p2p_peerload" = segment kernels load remote gradients from
-    peer memory (TIERSHARD_PULL_GRADS=0), "nccl" = staged NCCL all-to-allv
+    """exchange: "p2p" = peer-memory serve + gradient push (default on one
+    node), "p2p_pull" = servers gather remote gradients with peer loads
+    (TIERSHARD_GRADS=pull), "nccl" = staged NCCL all-to-allv
     (TIERSHARD_EXCHANGE=nccl)."""
     u = n_nodes * w
     if n_devices() < u:
@@ -66,7 +66,7 @@ def test_multi_gpu_matches_oracle(cuda, tmp_path, n_nodes, w, opt, exchange):
            str(ROOT / "tests" / "mg_worker.py"), "--nodes", str(n_nodes), "--gpus-per-node", str(w),
            "--optimizer", str(opt), "--lr", str(LR), "--out", str(tmp_path)]
     env = dict(os.environ, TIERSHARD_EXCHANGE="nccl" if exchange == "nccl" else "p2p",
-               TIERSHARD_PULL_GRADS="0" if exchange == "p2p_peerload" else "1")
+               TIERSHARD_GRADS="pull" if exchange == "p2p_pull" else "push")
     proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
     pb = mg_worker.problem(n_nodes, w)
@@ -135,6 +135,6 @@ def test_multi_gpu_host_steps_match_oracle(cuda, tmp_path, n_nodes, w, opt):
         orc.backward_update(w_ref, st_ref, allrows, orc.gather(w_ref, allrows), opt, LR_STEPS, 1e-8)
     for g in range(u):
         stored = res[g]["stored"]
-        np.testing.assert_allclose(res[g]["weights"], w_ref[stored], rtol=1e-6, atol=1e-9)
+        np.testing.assert_allclose(res[g]["weights"], w_ref[stored], rtol=1e-6, atol=1e-8)
     for g in range(1, u):
         assert np.array_equal(res[g]["weights"][:dp].view(np.uint32), res[0]["weights"][:dp].view(np.uint32))

@@ -1,16 +1,15 @@
 mkdir -p gpurun_out
-timeout 300 python bench.py --steps 20 --warmup 5 > gpurun_out/diag_n1.json 2> gpurun_out/diag_n1.err
-for N in 2 4; do
-TS_BENCH_DIAG=1 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29511 \
-  bench.py --gpus $N --steps 20 --warmup 5 > gpurun_out/diag_n$N.json 2> gpurun_out/diag_n$N.err
-done
-for N in 1 2 4; do
+TIERSHARD_PUSH_ORDER=first timeout 900 python -m pytest tests/test_gpu_multigpu.py -x -q -k "p2p" > gpurun_out/mg_tests.log 2>&1; echo rc=$? >> gpurun_out/mg_tests.log
+tail -2 gpurun_out/mg_tests.log
+for po in overlap first; do
+N=4
+TIERSHARD_PUSH_ORDER=$po TS_BENCH_DIAG=1 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29511 \
+  bench.py --gpus $N --steps 20 --warmup 5 --no-e2e > gpurun_out/diag_n4.json 2> gpurun_out/diag_n4.err
 python - <<PY
 import json
-d=json.loads([l for l in open('gpurun_out/diag_n$N.json') if l.startswith('{')][-1])
-e=d.get('e2e') or {}
-r=d['roofline']
-print('N=$N', d['value'], d['ms_per_step'], 'e2e', e.get('value'), e.get('step_wall_ms'), 'diag', e.get('diag_torch_buffers_value'), e.get('diag_host_api_pinned_value'))
-print('  ', r['all_phases_ms_per_step'])
+d=json.loads([l for l in open('gpurun_out/diag_n4.json') if l.startswith('{')][-1])
+print('push_order=$po', d['value'], d['ms_per_step'])
+for rk, tr in enumerate(d['step_trace_ms_all_ranks']):
+    print('rank', rk, ' '.join(f"{n}:{s}:{a:.2f}-{b:.2f}" for n, s, a, b in tr))
 PY
 done
