@@ -22,6 +22,7 @@
 
 struct ts_table;   // C-ABI handles
 struct ts_keymap;
+struct ts_sampler;
 
 namespace tiershard {
 
@@ -88,6 +89,27 @@ class KeyMap {
 
  private:
   ts_keymap* map_ = nullptr;
+};
+
+// GPU workload sampler (throughput runs; tiershard_b200.h ts_sampler_*): the
+// reference Workload's per-sample law (Poisson(L) length, alias draws over
+// the same AliasTable) on per-sample streams, so a U-GPU job can sample each
+// rank's samples on its own GPU.  Not the host Workload's stream.
+class DeviceSampler {
+ public:
+  DeviceSampler(const RowDistribution& dist, uint64_t seed, int device = 0);
+  ~DeviceSampler();
+  DeviceSampler(const DeviceSampler&) = delete;
+  DeviceSampler& operator=(const DeviceSampler&) = delete;
+
+  // Samples [sample_begin, sample_begin + samples) of `iteration` into d_rows
+  // (device, canonical rows) and d_offsets (device, samples + 1, optional).
+  // Returns the occurrence count; ValidationError beyond `capacity`.
+  uint64_t sample(uint32_t iteration, uint64_t sample_begin, uint32_t samples, uint32_t* d_rows,
+                  uint64_t capacity, uint64_t* d_offsets = nullptr, void* stream = nullptr);
+
+ private:
+  ts_sampler* sampler_ = nullptr;
 };
 
 // One rank's shard of the tiered table.  Collective when N*W > 1.

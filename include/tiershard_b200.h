@@ -138,6 +138,34 @@ ts_status ts_keymap_lookup(ts_keymap* m, const uint32_t* d_table_ids,
 ts_status ts_keymap_destroy(ts_keymap* m);
 
 /* ------------------------------------------------------------------------
+ * GPU workload sampler, for throughput runs.  Every
+ * sample follows the reference's per-sample procedure (Workload::
+ * materialize_iteration, simulator.cpp:54-71: a Poisson(L) length, then L
+ * alias draws; rng.cpp:15-115) on its own SplitMix64 stream seeded from
+ * (seed, iteration, sample), over the reference's alias table (built on the
+ * host, uploaded).  Same distribution as the host Workload, not the same
+ * stream: the host path stays the bit-exact one.
+ * ---------------------------------------------------------------------- */
+typedef struct ts_sampler ts_sampler;
+
+/* alias_prob / alias_index: the AliasTable of the canonical probabilities
+ * (tiershard::AliasTable::probabilities() / aliases()). */
+ts_status ts_sampler_create(ts_sampler** out, int device, uint64_t n_rows,
+                            const double* alias_prob, const uint32_t* alias_index,
+                            double expected_length, uint64_t seed);
+
+/* Samples [sample_begin, sample_begin + samples) of `iteration` (GPU g of a
+ * U-GPU job passes sample_begin = g * local_batch): canonical rows into
+ * d_rows (device), CSR offsets into d_offsets (device, samples + 1 entries,
+ * may be NULL), the occurrence count into *occurrences (host; the call
+ * synchronises once).  ValidationError when the rows exceed rows_capacity. */
+ts_status ts_sampler_iteration(ts_sampler* s, uint32_t iteration, uint64_t sample_begin,
+                               uint32_t samples, uint32_t* d_rows, uint64_t rows_capacity,
+                               uint64_t* d_offsets, uint64_t* occurrences, void* stream);
+
+ts_status ts_sampler_destroy(ts_sampler* s);
+
+/* ------------------------------------------------------------------------
  * Host-only planning helpers of the U > 1 path (no device needed).
  * ---------------------------------------------------------------------- */
 

@@ -12,6 +12,7 @@ from .capi import (  # noqa: F401
     TSError,
     Router,
     KeyMap,
+    Sampler,
     Table,
     load,
     build_info,

@@ -72,6 +72,9 @@ EXPORTS = (
     "ts_keymap_lookup",
     "ts_keymap_destroy",
     "ts_table_forward_keys",
+    "ts_sampler_create",
+    "ts_sampler_iteration",
+    "ts_sampler_destroy",
 )
 
 
@@ -158,6 +161,9 @@ def load() -> C.CDLL:
         "ts_keymap_lookup": (C.c_int, [vp, vp, vp, C.c_uint64, vp, vp, u64p]),
         "ts_keymap_destroy": (C.c_int, [vp]),
         "ts_table_forward_keys": (C.c_int, [vp, vp, vp, vp, C.c_uint64, vp]),
+        "ts_sampler_create": (C.c_int, [C.POINTER(vp), C.c_int, C.c_uint64, vp, vp, C.c_double, C.c_uint64]),
+        "ts_sampler_iteration": (C.c_int, [vp, C.c_uint32, C.c_uint64, C.c_uint32, vp, C.c_uint64, vp, u64p, vp]),
+        "ts_sampler_destroy": (C.c_int, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -283,6 +289,38 @@ class KeyMap:
     def close(self):
         if getattr(self, "_h", None):
             _check(self._lib.ts_keymap_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Sampler:
+    """ts_sampler_*: GPU workload sampler over an alias table (throughput runs)."""
+
+    def __init__(self, alias_prob: np.ndarray, alias_index: np.ndarray, expected_length: float,
+                 seed: int, device: int = 0):
+        self._lib = load()
+        p = np.ascontiguousarray(alias_prob, dtype=np.float64)
+        a = np.ascontiguousarray(alias_index, dtype=np.uint32)
+        h = vp()
+        _check(self._lib.ts_sampler_create(C.byref(h), device, p.size, _ptr(p) if p.size else None,
+                                           _ptr(a) if a.size else None, expected_length, seed))
+        self._h = h
+
+    def iteration(self, iteration: int, sample_begin: int, samples: int, d_rows: int, capacity: int,
+                  d_offsets: int = 0, stream: int = 0) -> int:
+        occ = C.c_uint64(0)
+        _check(self._lib.ts_sampler_iteration(self._h, iteration, sample_begin, samples, d_rows or None,
+                                              capacity, d_offsets or None, C.byref(occ), stream or None))
+        return occ.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _check(self._lib.ts_sampler_destroy(self._h))
             self._h = None
 
     def __del__(self):

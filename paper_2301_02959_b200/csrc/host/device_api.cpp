@@ -6,6 +6,7 @@
 #include "capi_check.hpp"
 #include "parallel.hpp"
 #include "tiershard/error.hpp"
+#include "tiershard/rng.hpp"
 #include "tiershard/simulator.hpp"
 #include "tiershard_b200.h"
 
@@ -98,6 +99,27 @@ uint64_t KeyMap::lookup(const uint32_t* d_table_ids, const uint64_t* d_row_ids, 
   uint64_t misses = 0;
   detail::check(ts_keymap_lookup(map_, d_table_ids, d_row_ids, n, d_canon, stream, &misses));
   return misses;
+}
+
+DeviceSampler::DeviceSampler(const RowDistribution& dist, uint64_t seed, int device) {
+  if (dist.rows().empty()) throw ValidationError("workload: distribution has no materialized rows");
+  std::vector<double> w(dist.rows().size());  // as Workload's constructor (simulator.cpp)
+  for (size_t i = 0; i < w.size(); ++i) w[i] = dist.rows()[i].probability;
+  const AliasTable table(w);
+  detail::check(ts_sampler_create(&sampler_, device, w.size(), table.probabilities().data(),
+                                  table.aliases().data(), dist.expected_length(), seed));
+}
+
+DeviceSampler::~DeviceSampler() {
+  if (sampler_) ts_sampler_destroy(sampler_);
+}
+
+uint64_t DeviceSampler::sample(uint32_t iteration, uint64_t sample_begin, uint32_t samples, uint32_t* d_rows,
+                               uint64_t capacity, uint64_t* d_offsets, void* stream) {
+  uint64_t occ = 0;
+  detail::check(ts_sampler_iteration(sampler_, iteration, sample_begin, samples, d_rows, capacity, d_offsets,
+                                     &occ, stream));
+  return occ;
 }
 
 void SequenceEmbedding::backward(const float* d_grad) { detail::check(ts_table_backward(table_, d_grad)); }

@@ -313,6 +313,16 @@ Json run(const Json& spec) {
                                                                           : placements[i].owner_gpu);
     }
     write_binary(dir + "/dest.u8", dest);
+    if (spec.value("export_alias", false)) {  // the Workload's alias table (GPU sampler input)
+      std::vector<double> w(d.rows().size());
+      for (size_t i = 0; i < w.size(); ++i) w[i] = d.rows()[i].probability;
+      const ts::AliasTable at(w);
+      const std::vector<double> prob(at.probabilities().begin(), at.probabilities().end());
+      const std::vector<uint32_t> idx(at.aliases().begin(), at.aliases().end());
+      write_binary(dir + "/alias.prob.f64", prob);
+      write_binary(dir + "/alias.idx.u32", idx);
+      out["expected_length"] = d.expected_length();
+    }
     const Json& jw = spec.at("workload");
     const uint32_t iters = jw.value("iterations", 1u);
     const ts::Workload wl = ts::sample_workload(dist, cfg, topo, jw.value("seed", uint64_t{7}), iters);
