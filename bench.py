@@ -60,6 +60,10 @@ def parse_args():
     p.add_argument("--virtual-nodes", action="store_true", help="2 x N/2 virtual nodes, paper bw, 3-tier")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--sampler", choices=("host", "gpu"), default="host",
+                   help="host: the reference Workload's batches (bit-exact), materialized once and "
+                        "cycled; gpu: each step's batch drawn on the GPU inside the timed region "
+                        "(ts_sampler, same law, for C4/C5-scale throughput runs)")
     p.add_argument("--cache", default="/tmp/tiershard_bench")
     return p.parse_args()
 
@@ -135,7 +139,9 @@ def workload_spec(args, n_gpus):
                    seed=1000 + t) for t in range(args.tables)]
     return dict(tables=tables, topology=topo,
                 cost_model=dict(local_batch=args.batch, embedding_dim=args.dim), goal=goal,
-                frontier=False, hash_seed=2, workload=dict(seed=7, iterations=args.iterations))
+                frontier=False, hash_seed=2,
+                workload=dict(seed=7, iterations=args.iterations if args.sampler == "host" else 1),
+                export_alias=args.sampler == "gpu")
 
 
 def prepare(args, dist: Dist, n_gpus):
@@ -281,6 +287,13 @@ def run_ours(args, dist: Dist):
         lo, hi = int(off[g * B]), int(off[(g + 1) * B])
         batches.append(np.ascontiguousarray(rows[lo:hi]))
     max_occ = max(b.size for b in batches)
+    sampler = None
+    if args.sampler == "gpu":
+        # capacity: the Poisson(L) batch total stays far below L*B + 8 sqrt(L*B)
+        L = float(doc["expected_length"])
+        max_occ = max(max_occ, int(L * B + 8 * np.sqrt(L * B)) + 1024)
+        sampler = ts.Sampler(np.fromfile(data_dir / "alias.prob.f64", np.float64),
+                             np.fromfile(data_dir / "alias.idx.u32", np.uint32), L, seed=7, device=device)
 
     nccl_id = None
     if u > 1:
@@ -296,7 +309,16 @@ def run_ours(args, dist: Dist):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{device}")  # 2x L2
     torch.cuda.synchronize()
 
+    if sampler is not None:
+        d_sampled = torch.empty(max_occ, dtype=torch.int32, device=f"cuda:{device}")
+        sampled_occ = []
+
     def step(k):
+        if sampler is not None:  # this rank's samples [g B, (g+1) B) of iteration k, on the GPU
+            occ = sampler.iteration(k, g * B, B, d_sampled.data_ptr(), max_occ, 0, table.stream())
+            sampled_occ.append(occ)
+            table.train_step(d_sampled.data_ptr(), occ, d_out.data_ptr())
+            return
         b = d_rows[k % len(d_rows)]
         table.train_step(b.data_ptr(), b.numel(), d_out.data_ptr())
 
@@ -328,8 +350,9 @@ def run_ours(args, dist: Dist):
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
     launches = ts.kernel_launches() - launches0
-    dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    dev_ms = dist.max(dev_ms)
+    per_step = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    step_ms_pct = [round(float(np.percentile(per_step, q)), 4) for q in (0, 50, 100)]
+    dev_ms = dist.max(sum(per_step))
     samples = u * B * args.steps
     value = samples / (dev_ms / 1e3)
     loss = table.loss()
@@ -499,21 +522,27 @@ def run_ours(args, dist: Dist):
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(dev_ms / args.steps, 4),
+        "step_ms_min_median_max_rank0": step_ms_pct,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32",
-        "data": "synthetic: reference synthesize_zipf (seeds 1000+t) + Workload (seed 7), materialized "
-                "bit-exactly by the product host API; weights seeded-hash init",
+        "data": ("synthetic: reference synthesize_zipf (seeds 1000+t) + Workload (seed 7), materialized "
+                 "bit-exactly by the product host API; weights seeded-hash init") if sampler is None else
+                ("synthetic: reference synthesize_zipf (seeds 1000+t); every step's batch drawn on the GPU "
+                 "inside the timed region (ts_sampler: the Workload's per-sample law over its alias table); "
+                 "weights seeded-hash init"),
         "config": {
-            "workload": f"C2: {args.tables} tables x {args.rows} rows x D={D} fp32, seq len {args.seq_len}"
+            "workload": f"{'C2' if (args.tables, args.rows, args.seq_len) == (8, 10_000_000, 128) else 'custom'}: "
+                        f"{args.tables} tables x {args.rows} rows x D={D} fp32, seq len {args.seq_len}"
                         f"/table, batch {B}/GPU, Zipf {args.exponent}",
             "topology": f"{u // w} x {w}" + (" virtual nodes, paper bw" if args.virtual_nodes else " homogeneous"),
             "plan": plan["goal"], "dp_cut": plan["dp_cut"], "flex_cut": plan["flex_cut"],
             "global_batch": u * B, "seq_len": args.seq_len * args.tables,
             "parallelism": f"row-sharded over {u} GPU(s): DP/Flex/RW tiers",
             "optimizer": args.optimizer, "l2": "flushed (256 MiB write) between timed steps, outside events",
-            "batches_cycled": len(batches), "occurrences_per_gpu_step": occ_mean,
+            "batches_cycled": len(batches) if sampler is None else "gpu-sampled per step",
+            "occurrences_per_gpu_step": occ_mean if sampler is None else float(np.mean(sampled_occ)),
         },
         "e2e": e2e,
         "gpu_launches": int(launches),

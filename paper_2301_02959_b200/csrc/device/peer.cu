@@ -272,10 +272,19 @@ void launch_pull_requests(const PullTable& t, uint32_t* recv_ids, uint32_t* recv
   TSD_LAUNCH_CHECK();
 }
 
+unsigned serve_blocks() {
+  static const unsigned v = [] {
+    const char* e = std::getenv("TIERSHARD_SERVE_BLOCKS");
+    const int b = e ? std::atoi(e) : 96;
+    return static_cast<unsigned>(std::min<int>(std::max(b, 1), static_cast<int>(kServeGrid)));
+  }();
+  return v;
+}
+
 void launch_serve_rows(const float* weights, const uint32_t* recv_ids, const uint32_t* recv_pos,
                        const ServeTable& st, uint32_t dim, cudaStream_t stream) {
   if (st.n == 0) return;
-  const dim3 grid(kServeGrid, st.n);
+  const dim3 grid(serve_blocks(), st.n);
   const uint32_t vec4 = (dim / 4 + 31) / 32;
   switch (vec4) {
     case 1: serve_rows_kernel<1><<<grid, kThreads, 0, stream>>>(weights, recv_ids, recv_pos, st, dim); break;

@@ -88,7 +88,10 @@ struct ServeTable {
   int n;
 };
 
-constexpr unsigned kServeGrid = 96;  // blocks per requester
+// Loss-slot stride per requester (the largest serve grid); the grid used is
+// serve_blocks() <= kServeGrid, fixed per process, so unused slots stay zero.
+constexpr unsigned kServeGrid = 512;
+unsigned serve_blocks();  // blocks per requester (TIERSHARD_SERVE_BLOCKS, default 96)
 
 // Remote gradient rows pulled into local HBM: dst[r] = src[s(r)][pos[r]]
 // where s(r) is the source whose range [src_start[s], src_start[s+1])

@@ -1,15 +1,17 @@
 mkdir -p gpurun_out
-TIERSHARD_PUSH_ORDER=first timeout 900 python -m pytest tests/test_gpu_multigpu.py -x -q -k "p2p" > gpurun_out/mg_tests.log 2>&1; echo rc=$? >> gpurun_out/mg_tests.log
-tail -2 gpurun_out/mg_tests.log
-for po in overlap first; do
-N=4
-TIERSHARD_PUSH_ORDER=$po TS_BENCH_DIAG=1 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29511 \
-  bench.py --gpus $N --steps 20 --warmup 5 --no-e2e > gpurun_out/diag_n4.json 2> gpurun_out/diag_n4.err
+run() {  # tag env...
+tag=$1; shift
+env "$@" TS_BENCH_DIAG=1 timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29511 \
+  bench.py --gpus 4 --steps 20 --warmup 5 --tables 16 --rows 25000000 --seq-len 256 --virtual-nodes --sampler gpu --no-e2e \
+  --cache /tmp/c4cache > gpurun_out/c4_$tag.json 2> gpurun_out/c4_$tag.err
 python - <<PY
 import json
-d=json.loads([l for l in open('gpurun_out/diag_n4.json') if l.startswith('{')][-1])
-print('push_order=$po', d['value'], d['ms_per_step'])
-for rk, tr in enumerate(d['step_trace_ms_all_ranks']):
-    print('rank', rk, ' '.join(f"{n}:{s}:{a:.2f}-{b:.2f}" for n, s, a, b in tr))
+d=json.loads([l for l in open('gpurun_out/c4_$tag.json') if l.startswith('{')][-1])
+print('$tag', d['value'], d['ms_per_step'], d['step_ms_min_median_max_rank0'], d['nvlink']['achieved_gbs'])
+print('  ', d['roofline']['all_phases_ms_per_step'])
 PY
-done
+}
+run base
+run push4 TIERSHARD_PUSH_BLOCKS=4
+run serve192 TIERSHARD_SERVE_BLOCKS=192
+run both TIERSHARD_PUSH_BLOCKS=4 TIERSHARD_SERVE_BLOCKS=192
