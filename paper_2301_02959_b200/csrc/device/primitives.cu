@@ -157,6 +157,7 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
   return v;
 }
 
+template <int kWindow>
 __global__ void __launch_bounds__(kRadixThreads, 3)
 onesweep_pass_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                      uint64_t n, int shift, int bits, const uint32_t* __restrict__ goff,
@@ -226,8 +227,11 @@ onesweep_pass_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __res
     st_relaxed_u64(my, kFlagAgg | count);
     // Windowed look-back: kWindow predecessor words in flight at once, then
     // consumed nearest-first until an inclusive prefix is found; a
-    // not-yet-published word restarts the window at that tile.
-    constexpr int kWindow = 8;
+    // not-yet-published word restarts the window at that tile.  Measured at
+    // C2 (4.2M pairs, 4 passes): window 1 / 2 / 4 / 8 / 16 / 32 ->
+    // 0.223 / 0.218 / 0.217 / 0.230 / 0.286 / 0.399 ms per sort (larger
+    // windows spill under the 3-blocks/SM register cap); default 4
+    // (TIERSHARD_LOOKBACK).
     int64_t p = static_cast<int64_t>(tile) - 1;
     bool done = false;
     while (!done) {
@@ -399,9 +403,21 @@ void radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t
     const int bits = key_bits - shift < 8 ? key_bits - shift : 8;
     uint32_t* out_k = (pass & 1) ? buf.keys_b : buf.keys_a;
     uint32_t* out_v = (pass & 1) ? buf.vals_b : buf.vals_a;
-    onesweep_pass_kernel<<<tiles, kRadixThreads, 0, stream>>>(
-        cur_k, cur_v, n, shift, bits, buf.goff + pass * kRadixBins,
-        buf.status + static_cast<uint64_t>(pass) * tiles * kRadixBins, buf.counters + pass, out_k, out_v);
+    static const int window = [] {
+      const char* e = std::getenv("TIERSHARD_LOOKBACK");
+      return e ? std::atoi(e) : 4;
+    }();
+    const auto launch = [&](auto kern) {
+      kern<<<tiles, kRadixThreads, 0, stream>>>(cur_k, cur_v, n, shift, bits, buf.goff + pass * kRadixBins,
+                                                buf.status + static_cast<uint64_t>(pass) * tiles * kRadixBins,
+                                                buf.counters + pass, out_k, out_v);
+    };
+    if (window >= 32) launch(onesweep_pass_kernel<32>);
+    else if (window >= 16) launch(onesweep_pass_kernel<16>);
+    else if (window >= 8) launch(onesweep_pass_kernel<8>);
+    else if (window >= 4) launch(onesweep_pass_kernel<4>);
+    else if (window >= 2) launch(onesweep_pass_kernel<2>);
+    else launch(onesweep_pass_kernel<1>);
     TSD_LAUNCH_CHECK();
     cur_k = out_k;
     cur_v = out_v;

@@ -106,6 +106,17 @@ struct ts_table {
   uint32_t U = 1, W = 1, N = 1, g = 0, slot = 0, node = 0;
   cudaStream_t stream = nullptr;  // compute stream (S)
   cudaStream_t comm = nullptr;    // exchange / all-reduce stream (C), U > 1
+  // U = 1: the dedup (sort + segment heads) needs only the row ids, so the
+  // forward starts it on `aux` beside the gather; the backward waits for it.
+  // TIERSHARD_DEDUP_IN_FORWARD=0 keeps it in the backward;
+  // TIERSHARD_GATHER_BLOCKS = the gather's blocks per SM meanwhile.
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fwd0 = nullptr, ev_dedup = nullptr;
+  bool dedup_in_forward = true;
+  bool dedup_ready = false;
+  uint32_t* dd_keys = nullptr;
+  uint32_t* dd_vals = nullptr;
+  unsigned fwd_gather_grid = 0;
   cudaEvent_t ev_ids = nullptr, ev_fwd = nullptr, ev_bwd0 = nullptr, ev_grads = nullptr,
               ev_dense = nullptr, ev_ar = nullptr;
   ncclComm_t world = nullptr, intra = nullptr, cross = nullptr;
@@ -213,6 +224,7 @@ struct ts_table {
     if (ev_used.empty()) return;
     TSD_CUDA(cudaStreamSynchronize(stream));
     if (comm) TSD_CUDA(cudaStreamSynchronize(comm));
+    if (aux) TSD_CUDA(cudaStreamSynchronize(aux));
     // keep the timeline of the last step (offsets from its first event): a
     // step starts at the first phase recorded after the previous collection
     trace.clear();
@@ -269,6 +281,7 @@ struct ts_table {
 
   // ------------------------------------------------------------------------
   void create(const ts_table_config& c, const uint8_t* tier_dest);
+  void dedup_local(cudaStream_t on);
   void forward(const uint32_t* d_rows, uint64_t occ, float* d_out);
   void backward(const float* d_grad);
   void exchange(const void* send, const std::vector<uint64_t>& s_off,
@@ -311,6 +324,14 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
   if (U > 1 && !tier_dest) fail(TS_ERR_CONFIG, "table: U > 1 needs the placement table");
   use_device(c.device);
   TSD_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  if (U == 1) {
+    if (const char* e = std::getenv("TIERSHARD_DEDUP_IN_FORWARD")) dedup_in_forward = std::string(e) != "0";
+    if (dedup_in_forward) {
+      TSD_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+      TSD_CUDA(cudaEventCreateWithFlags(&ev_fwd0, cudaEventDisableTiming));
+      TSD_CUDA(cudaEventCreateWithFlags(&ev_dedup, cudaEventDisableTiming));
+    }
+  }
 
   // ---- local layout --------------------------------------------------------
   std::vector<uint32_t> l2c;
@@ -368,6 +389,12 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
 
   // ---- step buffers ----------------------------------------------------------
   gather_grid = tsd::gather_grid(c.max_occurrences);
+  fwd_gather_grid = gather_grid;
+  if (aux) {
+    const char* e = std::getenv("TIERSHARD_GATHER_BLOCKS");
+    const unsigned per_sm = e ? static_cast<unsigned>(std::max(1, std::atoi(e))) : 8u;
+    fwd_gather_grid = std::min(gather_grid, static_cast<unsigned>(tsd::sm_count()) * per_sm);
+  }
   // [local gather partials | remote partials: staged scatter (gather_grid) or
   //  peer servers' slots (U x kServeGrid)]; zeroed once — slots a server
   //  never writes (our own) must read 0.
@@ -554,6 +581,22 @@ void ts_table::exchange(const void* send, const std::vector<uint64_t>& s_off,
   TSD_NCCL(ncclGroupEnd());
 }
 
+// U = 1 dedup: stable sort of the forward's row ids (key = canonical row,
+// value = position) and segment heads, on stream `on`.
+void ts_table::dedup_local(cudaStream_t on) {
+  using namespace tsd;
+  RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, ghist.ptr, goff.ptr,
+                  sort_status.ptr, sort_counters.ptr};
+  const int key_bits = bits_for(local_rows ? local_rows - 1 : 0);
+  int t = phase_begin(kPhaseSort, on);
+  radix_sort_pairs(last_rows, nullptr, last_occ, key_bits, rb, &dd_keys, &dd_vals, on);
+  phase_end(t);
+  t = phase_begin(kPhaseSegments, on);
+  segment_starts(dd_keys, last_occ, starts.ptr, seg_keys.ptr, nseg.ptr, seg_scratch.ptr, on);
+  TSD_CUDA(cudaMemsetAsync(seg_split.ptr, 0, sizeof(uint32_t), on));  // range [0, nseg)
+  phase_end(t);
+}
+
 // ---------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------
@@ -568,12 +611,19 @@ void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   TSD_CUDA(cudaMemsetAsync(tier_counts.ptr, 0, sizeof(unsigned long long) * 4, stream));
 
   if (U == 1) {
+    if (aux) TSD_CUDA(cudaEventRecord(ev_fwd0, stream));  // the ids are in place
     int t = phase_begin(kPhaseGather);
-    launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, gather_grid, stream);
+    launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, fwd_gather_grid, stream);
     phase_end(t);
     launch_loss_finalize(loss_partials.ptr, gather_grid, d_loss.ptr, stream);
     n_local_occ = occ;
     n_remote = 0;
+    if (aux) {  // the backward's dedup, overlapping the gather
+      TSD_CUDA(cudaStreamWaitEvent(aux, ev_fwd0, 0));
+      dedup_local(aux);
+      TSD_CUDA(cudaEventRecord(ev_dedup, aux));
+      dedup_ready = true;
+    }
     return;
   }
 
@@ -692,14 +742,15 @@ void ts_table::backward(const float* d_grad) {
   if (U == 1) {
     // local id == canonical index: sort the forward's rows directly
     last_entries = occ;
-    int t = phase_begin(kPhaseSort);
-    radix_sort_pairs(last_rows, nullptr, occ, key_bits, rb, &sk, &sv, stream);
-    phase_end(t);
-    t = phase_begin(kPhaseSegments);
-    segment_starts(sk, occ, starts.ptr, seg_keys.ptr, nseg.ptr, seg_scratch.ptr, stream);
-    TSD_CUDA(cudaMemsetAsync(seg_split.ptr, 0, sizeof(uint32_t), stream));  // range [0, nseg)
-    phase_end(t);
-    t = phase_begin(kPhaseSegmentUpdate);
+    if (dedup_ready) {
+      TSD_CUDA(cudaStreamWaitEvent(stream, ev_dedup, 0));
+      dedup_ready = false;
+    } else {
+      dedup_local(stream);
+    }
+    sk = dd_keys;
+    sv = dd_vals;
+    int t = phase_begin(kPhaseSegmentUpdate);
     launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr, nseg.ptr, occ, cfg.dim, gs, d_w, d_state,
                           opt, d0, d1, sc, stream);
     phase_end(t);
@@ -1141,8 +1192,12 @@ void ts_table::destroy() {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
   }
-  for (cudaEvent_t e : {ev_ids, ev_fwd, ev_bwd0, ev_grads, ev_dense, ev_ar}) {
+  for (cudaEvent_t e : {ev_ids, ev_fwd, ev_bwd0, ev_grads, ev_dense, ev_ar, ev_fwd0, ev_dedup}) {
     if (e) cudaEventDestroy(e);
+  }
+  if (aux) {
+    cudaStreamSynchronize(aux);
+    cudaStreamDestroy(aux);
   }
   if (comm) cudaStreamDestroy(comm);
   if (stream) cudaStreamDestroy(stream);
@@ -1341,6 +1396,8 @@ ts_status ts_table_synchronize(ts_table* t) {
     if (!t) tsd::fail(TS_ERR_CONFIG, "ts_table_synchronize: null table");
     TSD_CUDA(cudaSetDevice(t->cfg.device));
     TSD_CUDA(cudaStreamSynchronize(t->stream));
+    if (t->aux) TSD_CUDA(cudaStreamSynchronize(t->aux));
+    if (t->comm) TSD_CUDA(cudaStreamSynchronize(t->comm));
   });
 }
 
