@@ -282,6 +282,7 @@ struct ts_table {
   // ------------------------------------------------------------------------
   void create(const ts_table_config& c, const uint8_t* tier_dest);
   void dedup_local(cudaStream_t on);
+  void dedup_p2p(cudaStream_t on);
   void forward(const uint32_t* d_rows, uint64_t occ, float* d_out);
   void backward(const float* d_grad);
   void exchange(const void* send, const std::vector<uint64_t>& s_off,
@@ -324,7 +325,7 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
   if (U > 1 && !tier_dest) fail(TS_ERR_CONFIG, "table: U > 1 needs the placement table");
   use_device(c.device);
   TSD_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-  if (U == 1) {
+  {
     if (const char* e = std::getenv("TIERSHARD_DEDUP_IN_FORWARD")) dedup_in_forward = std::string(e) != "0";
     if (dedup_in_forward) {
       TSD_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
@@ -594,6 +595,31 @@ void ts_table::dedup_local(cudaStream_t on) {
   t = phase_begin(kPhaseSegments, on);
   segment_starts(dd_keys, last_occ, starts.ptr, seg_keys.ptr, nseg.ptr, seg_scratch.ptr, on);
   TSD_CUDA(cudaMemsetAsync(seg_split.ptr, 0, sizeof(uint32_t), on));  // range [0, nseg)
+  phase_end(t);
+}
+
+// U > 1 (peer path) dedup: (local row, source) entries of the local
+// occurrences and of the requests this rank serves, stable sort, segment
+// heads, and the replicated / rest split -- on stream `on`.  Needs the
+// forward's request lists (recv_ids), not the gradients.
+void ts_table::dedup_p2p(cudaStream_t on) {
+  using namespace tsd;
+  const uint64_t m = n_local_occ + recv_total;
+  entry_keys.ensure(m);
+  entry_vals.ensure(m);
+  ensure_sort_capacity(m);
+  launch_build_entries(last_rows, order.ptr + n_remote, n_local_occ, remap_view(), recv_ids.ptr, recv_before,
+                       recv_total, static_cast<uint32_t>(last_occ), entry_keys.ptr, entry_vals.ptr, on);
+  RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, ghist.ptr, goff.ptr,
+                  sort_status.ptr, sort_counters.ptr};
+  int t = phase_begin(kPhaseSort, on);
+  radix_sort_pairs(entry_keys.ptr, entry_vals.ptr, m, bits_for(local_rows ? local_rows - 1 : 0), rb, &dd_keys,
+                   &dd_vals, on);
+  phase_end(t);
+  t = phase_begin(kPhaseSegments, on);
+  segment_starts(dd_keys, m, starts.ptr, seg_keys.ptr, nseg.ptr, seg_scratch.ptr, on);
+  const uint32_t dense_hi = static_cast<uint32_t>(dp_rows + (N > 1 ? flex_rows : 0));
+  launch_segment_split(dd_keys, starts.ptr, nseg.ptr, dense_hi, seg_split.ptr, on);
   phase_end(t);
 }
 
@@ -939,8 +965,21 @@ void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
     tg.r_end = recv_off[2 * p] + recv_cnt[2 * p] + recv_cnt[2 * p + 1];
   }
   pt.total = recv_total;
+  if (aux) {  // buffers the aux dedup needs, sized before any of it is queued
+    const uint64_t m = n_local_occ + recv_total;
+    entry_keys.ensure(m);
+    entry_vals.ensure(m);
+    ensure_sort_capacity(m);
+  }
   t = phase_begin(kPhaseExchangeFwd, comm);
   launch_pull_requests(pt, recv_ids.ptr, recv_pos.ptr, comm);
+  if (aux) {  // the backward's dedup needs only the ids: overlap it with the gather / serve
+    TSD_CUDA(cudaEventRecord(ev_fwd0, comm));
+    TSD_CUDA(cudaStreamWaitEvent(aux, ev_fwd0, 0));
+    dedup_p2p(aux);
+    TSD_CUDA(cudaEventRecord(ev_dedup, aux));
+    dedup_ready = true;
+  }
   launch_serve_rows(d_w, recv_ids.ptr, recv_pos.ptr, st, cfg.dim, comm);
   barrier_on_comm();  // every server has finished storing into every output
   phase_end(t);
@@ -965,23 +1004,16 @@ void ts_table::backward_p2p(const float* d_grad) {
   DenseRange d0, d1;
   const uint64_t m = n_local_occ + recv_total;
   last_entries = m;
-  entry_keys.ensure(m);
-  entry_vals.ensure(m);
-  ensure_sort_capacity(m);
   SegmentScratch sc;
   sc.long_list = long_list.ptr;
   sc.long_count = long_count.ptr;
   sc.piece_off = piece_off.ptr;
   sc.partials = partials.ptr;
-  RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, ghist.ptr, goff.ptr,
-                  sort_status.ptr, sort_counters.ptr};
-  uint32_t* sk = nullptr;
-  uint32_t* sv = nullptr;
 
-  // ---- compute stream: entries, sort, segments (no gradient needed yet) ---
+  // ---- entries, sort, segments (no gradient needed): done by the forward on
+  // the aux stream when prefetched, else here on the compute stream -------
   TSD_CUDA(cudaEventRecord(ev_bwd0, stream));  // our gradient is complete here
-  launch_build_entries(last_rows, order.ptr + n_remote, n_local_occ, rv, recv_ids.ptr, recv_before,
-                       recv_total, static_cast<uint32_t>(occ), entry_keys.ptr, entry_vals.ptr, stream);
+  const bool prefetched = dedup_ready;
   // replicated rows' partials are pushed to their owners' receive slots and
   // stamped with the step's epoch (no clears; untouched slots are ignored)
   if (++epoch == 0) epoch = 1;  // (2^32 steps) 0 is the initial stamp
@@ -1068,15 +1100,15 @@ void ts_table::backward_p2p(const float* d_grad) {
     TSD_CUDA(cudaEventRecord(ev_grads, comm));
   };
   if (push_first) exchange_grads(stream);
-  int t = phase_begin(kPhaseSort);
-  radix_sort_pairs(entry_keys.ptr, entry_vals.ptr, m, bits_for(local_rows ? local_rows - 1 : 0), rb, &sk, &sv,
-                   stream);
-  phase_end(t);
-  t = phase_begin(kPhaseSegments);
-  segment_starts(sk, m, starts.ptr, seg_keys.ptr, nseg.ptr, seg_scratch.ptr, stream);
-  const uint32_t dense_hi = static_cast<uint32_t>(dp_rows + (N > 1 ? flex_rows : 0));
-  launch_segment_split(sk, starts.ptr, nseg.ptr, dense_hi, seg_split.ptr, stream);
-  phase_end(t);
+  if (prefetched) {
+    TSD_CUDA(cudaStreamWaitEvent(stream, ev_dedup, 0));
+    dedup_ready = false;
+  } else {
+    dedup_p2p(stream);
+  }
+  uint32_t* sk = dd_keys;
+  uint32_t* sv = dd_vals;
+  int t = -1;
 
   if (!push_first) exchange_grads(comm);
   GradSource gs;
