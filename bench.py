@@ -177,16 +177,18 @@ class ClockSampler:
               "clocks_event_reasons.sw_power_cap")
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, device: int):
-        self.device = device
+    # One sampler per job (rank 0) over every GPU of the job: per-rank
+    # nvidia-smi pollers at 50 ms added driver-query stalls to the timed steps.
+    def __init__(self, devices):
+        self.devices = ",".join(str(d) for d in devices)
         self.proc = None
         self.lines = []
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                ["nvidia-smi", "-i", self.devices, f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -324,8 +326,9 @@ def run_ours(args, dist: Dist):
 
     # clocks are sampled from the warm-up through the e2e pass (the timed
     # region is inside that window; only samples under load are reported)
-    clocks = ClockSampler(device)
-    clocks.start()
+    clocks = ClockSampler(range(int(os.environ.get("LOCAL_WORLD_SIZE", u)))) if g == 0 else None
+    if clocks:
+        clocks.start()
     for k in range(args.warmup):
         step(k)
     table.synchronize()
@@ -423,7 +426,7 @@ def run_ours(args, dist: Dist):
         table.phase_times()
         e2e["step_trace_ms"] = [(n, sid, round(a, 4), round(b, 4)) for n, sid, a, b in table.phase_trace()]
         table.enable_timing(False)
-    clk = clocks.stop()
+    clk = clocks.stop() if clocks else None
 
     # ---- roofline of the dominant kernel -----------------------------------
     row_bytes = D * 4
