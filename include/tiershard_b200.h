@@ -254,6 +254,13 @@ ts_status ts_table_train_step_host(ts_table* t, const uint32_t* h_rows,
                                    uint64_t occ, double* h_loss);
 
 /* Loss of the last train step (synchronises the table stream). */
+/* `steps` host-buffer steps in one call (h_rows[s] / occ[s] = step s's batch
+ * in pinned host memory; h_losses[s] receives its loss, may be NULL).  Same
+ * math as calling ts_table_train_step_host once per step, pipelined: step
+ * s+1's host-to-device copy runs on a copy stream while step s computes. */
+ts_status ts_table_train_steps_host(ts_table* t, const uint32_t* const* h_rows, const uint64_t* occ,
+                                   uint32_t steps, double* h_losses);
+
 ts_status ts_table_loss(ts_table* t, double* loss);
 
 /* This rank's counter contribution for the last forward/backward: for the

@@ -75,6 +75,7 @@ EXPORTS = (
     "ts_sampler_create",
     "ts_sampler_iteration",
     "ts_sampler_destroy",
+    "ts_table_train_steps_host",
 )
 
 
@@ -164,6 +165,7 @@ def load() -> C.CDLL:
         "ts_sampler_create": (C.c_int, [C.POINTER(vp), C.c_int, C.c_uint64, vp, vp, C.c_double, C.c_uint64]),
         "ts_sampler_iteration": (C.c_int, [vp, C.c_uint32, C.c_uint64, C.c_uint32, vp, C.c_uint64, vp, u64p, vp]),
         "ts_sampler_destroy": (C.c_int, [vp]),
+        "ts_table_train_steps_host": (C.c_int, [vp, vp, vp, C.c_uint32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -376,6 +378,16 @@ class Table:
         _check(self._lib.ts_table_train_step_host(self._h, _ptr(r) if r.size else None, r.size,
                                                   C.byref(loss)))
         return loss.value
+
+    def train_steps_host(self, batches) -> np.ndarray:
+        """Pipelined host-buffer steps (ts_table_train_steps_host): one loss per batch."""
+        arrs = [np.ascontiguousarray(b, dtype=np.uint32) for b in batches]
+        ptrs = (vp * len(arrs))(*[(_ptr(a) if a.size else None) for a in arrs])
+        occ = np.array([a.size for a in arrs], dtype=np.uint64)
+        losses = np.zeros(len(arrs), dtype=np.float64)
+        _check(self._lib.ts_table_train_steps_host(self._h, ptrs, _ptr(occ) if occ.size else None, len(arrs),
+                                                   _ptr(losses) if losses.size else None))
+        return losses
 
     def loss(self) -> float:
         v = C.c_double(0.0)

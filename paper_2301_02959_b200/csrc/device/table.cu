@@ -140,6 +140,13 @@ struct ts_table {
   tsd::DevBuf<unsigned long long> tier_counts;  // RW, Flex, DP of this requester
   tsd::DevBuf<uint32_t> rows_dev;                // host-step staging
   tsd::DevBuf<float> host_out;                   // host-step output [max_occurrences x D]
+  // pipelined host steps (ts_table_train_steps_host): second id buffer, copy
+  // stream, per-buffer events, pinned loss landing area
+  tsd::DevBuf<uint32_t> rows_dev2;
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
+  double* h_loss_pinned = nullptr;
+  uint32_t h_loss_cap = 0;
   // dedup / sort
   tsd::DevBuf<uint32_t> keys_a, vals_a, keys_b, vals_b, ghist, goff, sort_counters;
   tsd::DevBuf<uint64_t> sort_status;
@@ -1231,6 +1238,15 @@ void ts_table::destroy() {
     cudaStreamSynchronize(aux);
     cudaStreamDestroy(aux);
   }
+  if (copy) {
+    cudaStreamSynchronize(copy);
+    cudaStreamDestroy(copy);
+  }
+  for (cudaEvent_t e : {ev_copied[0], ev_copied[1], ev_consumed[0], ev_consumed[1]}) {
+    if (e) cudaEventDestroy(e);
+  }
+  rows_dev2.release();
+  if (h_loss_pinned) cudaFreeHost(h_loss_pinned);
   if (comm) cudaStreamDestroy(comm);
   if (stream) cudaStreamDestroy(stream);
 }
@@ -1326,6 +1342,66 @@ ts_status ts_table_train_step_host(ts_table* t, const uint32_t* h_rows, uint64_t
     TSD_CUDA(cudaMemcpyAsync(&loss, t->d_loss.ptr, sizeof(double), cudaMemcpyDeviceToHost, t->stream));
     TSD_CUDA(cudaStreamSynchronize(t->stream));
     if (h_loss) *h_loss = loss;
+  });
+}
+
+ts_status ts_table_train_steps_host(ts_table* t, const uint32_t* const* h_rows, const uint64_t* occ,
+                                   uint32_t steps, double* h_losses) {
+  return tsd::guarded([&] {
+    using namespace tsd;
+    if (!t || (steps && (!h_rows || !occ))) tsd::fail(TS_ERR_CONFIG, "ts_table_train_steps_host: null argument");
+    TSD_CUDA(cudaSetDevice(t->cfg.device));
+    for (uint32_t s = 0; s < steps; ++s) {
+      if (occ[s] > t->cfg.max_occurrences) {
+        tsd::fail(TS_ERR_VALIDATION, "ts_table_train_steps_host: occurrences exceed max_occurrences");
+      }
+      if (occ[s] && !h_rows[s]) tsd::fail(TS_ERR_CONFIG, "ts_table_train_steps_host: null batch");
+    }
+    if (steps == 0) return;
+    // buffers that never move (peers map the output), created once
+    t->rows_dev.ensure(t->cfg.max_occurrences);
+    t->rows_dev2.ensure(t->cfg.max_occurrences);
+    t->host_out.ensure(t->cfg.max_occurrences * t->cfg.dim);
+    if (!t->copy) {
+      TSD_CUDA(cudaStreamCreateWithFlags(&t->copy, cudaStreamNonBlocking));
+      for (int b = 0; b < 2; ++b) {
+        TSD_CUDA(cudaEventCreateWithFlags(&t->ev_copied[b], cudaEventDisableTiming));
+        TSD_CUDA(cudaEventCreateWithFlags(&t->ev_consumed[b], cudaEventDisableTiming));
+        TSD_CUDA(cudaEventRecord(t->ev_consumed[b], t->stream));
+      }
+    }
+    if (steps > t->h_loss_cap) {
+      if (t->h_loss_pinned) TSD_CUDA(cudaFreeHost(t->h_loss_pinned));
+      t->h_loss_pinned = nullptr;
+      t->h_loss_cap = 0;
+      TSD_CUDA(cudaHostAlloc(&t->h_loss_pinned, sizeof(double) * steps, cudaHostAllocDefault));
+      t->h_loss_cap = steps;
+    }
+    uint32_t* buf[2] = {t->rows_dev.ptr, t->rows_dev2.ptr};
+    // step s's ids go to buffer s % 2 on the copy stream once step s-2 (the
+    // buffer's last reader) has finished; the copy of step s+1 is queued
+    // before step s's compute, so it overlaps it
+    const auto stage = [&](uint32_t s) {
+      const int b = static_cast<int>(s & 1u);
+      TSD_CUDA(cudaStreamWaitEvent(t->copy, t->ev_consumed[b], 0));
+      if (occ[s]) {
+        TSD_CUDA(cudaMemcpyAsync(buf[b], h_rows[s], sizeof(uint32_t) * occ[s], cudaMemcpyHostToDevice, t->copy));
+      }
+      TSD_CUDA(cudaEventRecord(t->ev_copied[b], t->copy));
+    };
+    stage(0);
+    for (uint32_t s = 0; s < steps; ++s) {
+      if (s + 1 < steps) stage(s + 1);
+      const int b = static_cast<int>(s & 1u);
+      TSD_CUDA(cudaStreamWaitEvent(t->stream, t->ev_copied[b], 0));
+      t->forward(buf[b], occ[s], t->host_out.ptr);
+      t->backward(t->host_out.ptr);
+      TSD_CUDA(cudaEventRecord(t->ev_consumed[b], t->stream));
+      TSD_CUDA(cudaMemcpyAsync(t->h_loss_pinned + s, t->d_loss.ptr, sizeof(double), cudaMemcpyDeviceToHost,
+                               t->stream));
+    }
+    TSD_CUDA(cudaStreamSynchronize(t->stream));
+    if (h_losses) std::memcpy(h_losses, t->h_loss_pinned, sizeof(double) * steps);
   });
 }
 

@@ -43,6 +43,7 @@ def main():
     ap.add_argument("--optimizer", type=int, default=1)
     ap.add_argument("--lr", type=float, default=1e-3)
     ap.add_argument("--steps", type=int, default=1, help="> 1: host-buffer steps (train_step_host)")
+    ap.add_argument("--pipelined", action="store_true", help="the steps in one train_steps_host call")
     ap.add_argument("--out", required=True)
     args = ap.parse_args()
     import torch
@@ -64,7 +65,10 @@ def main():
                      max_occurrences=int(max(r[rank].size for r in pb["steps_rows"])),
                      nccl_unique_id=box[0])
     if args.steps > 1:
-        losses = [table.train_step_host(r[rank]) for r in pb["steps_rows"]]
+        if args.pipelined:
+            losses = list(table.train_steps_host([r[rank] for r in pb["steps_rows"]]))
+        else:
+            losses = [table.train_step_host(r[rank]) for r in pb["steps_rows"]]
         out = np.zeros((0, pb["dim"]), np.float32)
         loss = np.array(losses)
     else:

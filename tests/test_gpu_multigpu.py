@@ -106,8 +106,9 @@ def test_multi_gpu_matches_oracle(cuda, tmp_path, n_nodes, w, opt, exchange):
         assert np.array_equal(res[g]["weights"][:dp].view(np.uint32), res[0]["weights"][:dp].view(np.uint32))
 
 
-@pytest.mark.parametrize("n_nodes,w,opt", [(1, 2, 1), (2, 2, 1), (1, 4, 0)])
-def test_multi_gpu_host_steps_match_oracle(cuda, tmp_path, n_nodes, w, opt):
+@pytest.mark.parametrize("n_nodes,w,opt,pipelined", [(1, 2, 1, False), (2, 2, 1, False), (1, 4, 0, False),
+                                                     (1, 2, 1, True), (2, 2, 1, True)])
+def test_multi_gpu_host_steps_match_oracle(cuda, tmp_path, n_nodes, w, opt, pipelined):
     """Three steps through the host-buffer entry point (ts_table_train_step_host)
     with batches growing step to step: every step's loss and the final weights
     follow the oracle's sequential updates (stale peer mappings or stale
@@ -120,6 +121,8 @@ def test_multi_gpu_host_steps_match_oracle(cuda, tmp_path, n_nodes, w, opt):
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
            str(ROOT / "tests" / "mg_worker.py"), "--nodes", str(n_nodes), "--gpus-per-node", str(w),
            "--optimizer", str(opt), "--lr", str(LR_STEPS), "--steps", str(steps), "--out", str(tmp_path)]
+    if pipelined:
+        cmd.append("--pipelined")
     proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
     pb = mg_worker.problem(n_nodes, w, steps=steps)

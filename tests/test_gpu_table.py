@@ -96,6 +96,33 @@ def test_two_steps_and_host_entry(cuda):
     assert np.array_equal(got.view(np.uint32), w.view(np.uint32))
 
 
+def test_pipelined_host_steps_match_oracle(cuda):
+    """ts_table_train_steps_host: five steps (different sizes, one empty) in one
+    pipelined call -- every loss and the final weights bit-exact with the
+    oracle's sequential steps."""
+    import paper_2301_02959_b200 as ts
+    rng = np.random.default_rng(11)
+    n, dim = 4000, 64
+    sizes = [9000, 12000, 0, 7000, 12000]
+    lr = 0.05
+    table = ts.Table(n_rows=n, dim=dim, dp_cut=0, flex_cut=0, weight_seed=SEED,
+                     optimizer=orc.OPT_ROWWISE_ADAGRAD, lr=lr, max_occurrences=max(sizes))
+    batches = [zipf_rows(rng, n, k) if k else np.zeros(0, np.uint32) for k in sizes]
+    losses = table.train_steps_host(batches)
+    w = orc.init_table(SEED, n, dim)
+    state = np.zeros(n, np.float32)
+    for b, loss in zip(batches, losses):
+        expect = orc.gather(w, b) if b.size else np.zeros((0, dim), np.float32)
+        assert loss == pytest.approx(orc.half_sq_sum(expect), rel=1e-6, abs=1e-12)
+        if b.size:
+            orc.backward_update(w, state, b, expect, orc.OPT_ROWWISE_ADAGRAD, lr, 1e-8)
+    got = table.read_rows(np.arange(n, dtype=np.uint32))
+    assert np.array_equal(got.view(np.uint32), w.view(np.uint32))
+    with pytest.raises(ts.TSError) as e:
+        table.train_steps_host([np.zeros(max(sizes) + 1, np.uint32)])
+    assert e.value.kind == "ValidationError"
+
+
 def test_edge_cases(cuda):
     import paper_2301_02959_b200 as ts
     n, dim = 1000, 64
