@@ -448,7 +448,7 @@ seg_pair_kernel(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ 
                 const uint32_t* __restrict__ seg_keys, const uint32_t* __restrict__ d_lo,
                 const uint32_t* __restrict__ d_hi, GradSource gs, float* __restrict__ weights,
                 float* __restrict__ state, OptParams opt, DenseRange d0, DenseRange d1,
-                uint32_t* __restrict__ long_list, uint32_t* __restrict__ long_count) {
+                uint32_t* __restrict__ long_list, uint32_t* __restrict__ long_count, uint32_t short_max) {
   constexpr int PER = Grp<DIM, G>::PER;
   const unsigned lane = threadIdx.x & 31u;
   const unsigned group = lane / G, gl = lane % G;
@@ -465,7 +465,7 @@ seg_pair_kernel(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ 
     const uint32_t sa = __ldg(starts + ja), ea = __ldg(starts + ja + 1), ka = __ldg(seg_keys + ja);
     const uint32_t sb = has_b ? __ldg(starts + jb) : 0u, eb = has_b ? __ldg(starts + jb + 1) : 0u;
     const uint32_t kb = has_b ? __ldg(seg_keys + jb) : 0u;
-    const bool long_a = ea - sa > kPiece, long_b = has_b && eb - sb > kPiece;
+    const bool long_a = ea - sa > short_max, long_b = has_b && eb - sb > short_max;
     if (gl == 0) {
       if (long_a) long_list[atomicAdd(long_count, 1u)] = ja;
       if (long_b) long_list[atomicAdd(long_count, 1u)] = jb;
@@ -517,7 +517,7 @@ seg_short_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__
                  const uint32_t* __restrict__ d_hi,
                  GradSource gs, float* __restrict__ weights, float* __restrict__ state,
                  OptParams opt, DenseRange d0, DenseRange d1, uint32_t* __restrict__ long_list,
-                 uint32_t* __restrict__ long_count) {
+                 uint32_t* __restrict__ long_count, uint32_t short_max) {
   using Gp = Grouping<DIM>;
   constexpr int G = Gp::G, PER = Gp::PER, E = Gp::E;
   const unsigned lane = threadIdx.x & 31u;
@@ -529,7 +529,7 @@ seg_short_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__
   const uint64_t col = static_cast<uint64_t>(gl) * PER;
   for (uint32_t j = seg_lo + gid; j < seg_hi; j += ngroups) {
     const uint32_t s = __ldg(starts + j), e = __ldg(starts + j + 1);
-    if (e - s > kPiece) {
+    if (e - s > short_max) {
       if (gl == 0) long_list[atomicAdd(long_count, 1u)] = j;
       continue;
     }
@@ -582,9 +582,11 @@ long_prefix_kernel(const uint32_t* __restrict__ long_list, const uint32_t* __res
 
 template <int DIM>
 __global__ void __launch_bounds__(kThreads)
-piece_kernel(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ starts,
-             const uint32_t* __restrict__ long_list, const uint32_t* __restrict__ long_count,
-             const uint32_t* __restrict__ piece_off, GradSource gs, float* __restrict__ partials) {
+piece_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+             const uint32_t* __restrict__ starts, const uint32_t* __restrict__ long_list,
+             const uint32_t* __restrict__ long_count, const uint32_t* __restrict__ piece_off, GradSource gs,
+             float* __restrict__ partials, float* __restrict__ weights, float* __restrict__ state, OptParams opt,
+             DenseRange d0, DenseRange d1) {
   constexpr int VEC = DIM / 32;
   const unsigned lane = threadIdx.x & 31u;
   const uint32_t n = *long_count;
@@ -603,8 +605,16 @@ piece_kernel(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ sta
     const uint32_t e = min(s + kPiece, seg_e);
     float acc[VEC];
     sum_entries<DIM>(vals, s, e, gs, acc);
-    store_lane<VEC>(partials + static_cast<uint64_t>(p) * DIM + lane * VEC, acc);
+    if (piece_off[lo + 1] - piece_off[lo] == 1) {
+      // a single-piece segment (a mid-length one the short kernel handed
+      // over): its sum is complete -- the same left-to-right order as the
+      // short path -- so apply it here
+      finish_row<DIM>(keys[seg_s], acc, weights, state, opt, d0, d1);
+    } else {
+      store_lane<VEC>(partials + static_cast<uint64_t>(p) * DIM + lane * VEC, acc);
+    }
   }
+  if (d0.push_n | d1.push_n) __threadfence_system();  // partials stored to peers
 }
 
 template <int DIM>
@@ -623,6 +633,7 @@ long_combine_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restric
   for (uint32_t i = gwarp; i < n; i += nwarps) {
     const uint32_t j = long_list[i];
     const uint32_t p0 = piece_off[i], p1 = piece_off[i + 1];
+    if (p1 - p0 == 1) continue;  // applied by piece_kernel
     float acc[VEC];
     load_lane<VEC>(partials + static_cast<uint64_t>(p0) * DIM + lane * VEC, acc);
     uint32_t p = p0 + 1;
@@ -848,6 +859,20 @@ int seg_variant() {
   }();
   return v;
 }
+// Segments longer than short_max() entries go to the warp-per-piece path
+// (TIERSHARD_SHORT_MAX, <= kPiece): the short kernel's 4-8 segments per warp
+// finish together only when their lengths are alike.  Same sums either way
+// (a single piece is summed left to right).  Measured at C2, N=1 (segment
+// update + long path, ms): 256 -> 0.712, 64 -> 0.693, 32 -> 0.684,
+// 16 -> 0.724, 8 -> 0.747.
+uint32_t short_max() {
+  static const uint32_t v = [] {
+    const char* e = std::getenv("TIERSHARD_SHORT_MAX");
+    const int x = e ? std::atoi(e) : 32;
+    return static_cast<uint32_t>(std::min<int>(std::max(x, 1), static_cast<int>(kPiece)));
+  }();
+  return v;
+}
 int seg_group_128() {
   static const int v = [] {
     const char* e = std::getenv("TIERSHARD_SEG_G");
@@ -870,18 +895,18 @@ void launch_segment_update(const uint32_t* keys, const uint32_t* vals, const uin
     if (seg_variant() == 0 || DIM > 128) {
       seg_short_kernel<DIM><<<grid, kThreads, 0, stream>>>(keys, vals, starts, d_lo, d_hi, grads,
                                                            weights, state, opt, dense0, dense1,
-                                                           sc.long_list, sc.long_count);
+                                                           sc.long_list, sc.long_count, short_max());
     } else if (DIM == 128 && seg_group_128() == 16) {
       if constexpr (DIM == 128) {
         seg_pair_kernel<DIM, 16><<<grid, kThreads, 0, stream>>>(vals, starts, seg_keys, d_lo, d_hi, grads,
                                                                weights, state, opt, dense0, dense1,
-                                                               sc.long_list, sc.long_count);
+                                                               sc.long_list, sc.long_count, short_max());
       }
     } else {
       constexpr int G = 8;  // DIM <= 128 here
       if constexpr (DIM <= 128) seg_pair_kernel<DIM, G><<<grid, kThreads, 0, stream>>>(vals, starts, seg_keys, d_lo, d_hi, grads,
                                                             weights, state, opt, dense0, dense1,
-                                                            sc.long_list, sc.long_count);
+                                                            sc.long_list, sc.long_count, short_max());
     }
     TSD_LAUNCH_CHECK();
   });
@@ -897,8 +922,9 @@ void launch_segment_long(const uint32_t* keys, const uint32_t* vals, const uint3
     constexpr int DIM = decltype(D)::value;
     long_prefix_kernel<<<1, 1024, 0, stream>>>(sc.long_list, sc.long_count, starts, sc.piece_off);
     TSD_LAUNCH_CHECK();
-    piece_kernel<DIM><<<grid, kThreads, 0, stream>>>(vals, starts, sc.long_list, sc.long_count,
-                                                     sc.piece_off, grads, sc.partials);
+    piece_kernel<DIM><<<grid, kThreads, 0, stream>>>(keys, vals, starts, sc.long_list, sc.long_count,
+                                                     sc.piece_off, grads, sc.partials, weights, state, opt,
+                                                     dense0, dense1);
     TSD_LAUNCH_CHECK();
     long_combine_kernel<DIM><<<grid, kThreads, 0, stream>>>(keys, starts, sc.long_list,
                                                             sc.long_count, sc.piece_off,

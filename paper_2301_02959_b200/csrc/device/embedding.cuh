@@ -11,6 +11,8 @@ namespace tsd {
 
 // Pieces of a long segment: ORC_PIECE in the oracle.
 constexpr uint32_t kPiece = 256;
+// Segments longer than this (<= kPiece) take the warp-per-piece path.
+uint32_t short_max();
 
 // How a requester finds the local shard row of a canonical row (or learns it
 // is served remotely).  identity: U == 1, local id == canonical index.

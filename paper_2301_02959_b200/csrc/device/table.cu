@@ -280,7 +280,7 @@ struct ts_table {
     starts.ensure(m + 1);
     seg_keys.ensure(m + 1);
     seg_scratch.ensure(tsd::segment_scratch_elems(m) + 8);
-    const uint64_t max_long = m / (tsd::kPiece + 1) + 1;
+    const uint64_t max_long = m / (tsd::short_max() + 1) + 1;
     long_list.ensure(max_long);
     piece_off.ensure(max_long + 1);
     partials.ensure((m / tsd::kPiece + max_long + 1) * cfg.dim);
