@@ -97,19 +97,25 @@ constexpr uint64_t kFlagAgg = 1ull << 62;   // tile-local count published
 constexpr uint64_t kFlagInc = 2ull << 62;   // inclusive prefix published
 constexpr uint64_t kCountMask = (1ull << 62) - 1;
 
-__device__ __forceinline__ int pass_bits(int key_bits, int pass) {
-  const int left = key_bits - 8 * pass;
-  return left < 8 ? left : 8;
+// Digit width of a sort: 8 bits (256 bins), or 9 bits (512 bins) when that
+// saves a pass (25..27-bit keys: 3 passes instead of 4).
+__device__ __forceinline__ int pass_bits(int key_bits, int pass, int digit_bits) {
+  const int left = key_bits - digit_bits * pass;
+  return left < digit_bits ? left : digit_bits;
 }
 
 // Digit histograms of every pass from ONE read of the keys.  Warps whose
 // digits all agree add 32 at once; otherwise plain shared atomics (few
 // conflicts when digits are spread).
+template <int BINS>
 __global__ void __launch_bounds__(kRadixThreads)
 onesweep_hist_kernel(const uint32_t* __restrict__ keys, uint64_t n, int key_bits, int passes,
                      uint32_t* __restrict__ ghist) {
-  __shared__ uint32_t s_h[kMaxRadixPasses][kRadixBins];
-  for (int p = 0; p < passes; ++p) s_h[p][threadIdx.x] = 0;
+  constexpr int DIGIT_BITS = BINS == 512 ? 9 : 8;
+  __shared__ uint32_t s_h[kMaxRadixPasses][BINS];
+  for (int p = 0; p < passes; ++p) {
+    for (int b = threadIdx.x; b < BINS; b += kRadixThreads) s_h[p][b] = 0;
+  }
   __syncthreads();
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRadixTile;
   const unsigned lane = threadIdx.x & 31u;
@@ -120,11 +126,11 @@ onesweep_hist_kernel(const uint32_t* __restrict__ keys, uint64_t n, int key_bits
     key[k] = i < n ? __ldg(keys + i) : 0u;
   }
   for (int p = 0; p < passes; ++p) {
-    const uint32_t mask = (1u << pass_bits(key_bits, p)) - 1u;
+    const uint32_t mask = (1u << pass_bits(key_bits, p, DIGIT_BITS)) - 1u;
 #pragma unroll
     for (int k = 0; k < kRadixItems; ++k) {
       const bool valid = base + static_cast<uint64_t>(k) * kRadixThreads + threadIdx.x < n;
-      const uint32_t d = (key[k] >> (8 * p)) & mask;
+      const uint32_t d = (key[k] >> (DIGIT_BITS * p)) & mask;
       if (warp_uniform(d, valid)) {
         if (lane == 0) atomicAdd(&s_h[p][d], 32u);
       } else if (valid) {
@@ -134,18 +140,33 @@ onesweep_hist_kernel(const uint32_t* __restrict__ keys, uint64_t n, int key_bits
   }
   __syncthreads();
   for (int p = 0; p < passes; ++p) {
-    if (s_h[p][threadIdx.x]) atomicAdd(ghist + p * kRadixBins + threadIdx.x, s_h[p][threadIdx.x]);
+    for (int b = threadIdx.x; b < BINS; b += kRadixThreads) {
+      if (s_h[p][b]) atomicAdd(ghist + p * BINS + b, s_h[p][b]);
+    }
   }
 }
 
-// Exclusive scan of each pass's 256 digit totals (one block per pass).
+// Exclusive scan of each pass's digit totals (one block per pass; thread t
+// owns the BINS/256 consecutive digits t*DPT ..).
+template <int BINS>
 __global__ void __launch_bounds__(kRadixThreads)
 onesweep_offsets_kernel(const uint32_t* __restrict__ ghist, uint32_t* __restrict__ goff) {
+  constexpr int DPT = BINS / kRadixThreads;
   __shared__ uint32_t s_warp[kRadixThreads / 32 + 1];
   const int p = blockIdx.x;
+  uint32_t v[DPT], sum = 0;
+#pragma unroll
+  for (int k = 0; k < DPT; ++k) {
+    v[k] = ghist[p * BINS + threadIdx.x * DPT + k];
+    sum += v[k];
+  }
   uint32_t total;
-  goff[p * kRadixBins + threadIdx.x] =
-      block_exclusive_scan<kRadixThreads>(ghist[p * kRadixBins + threadIdx.x], s_warp, &total);
+  uint32_t run = block_exclusive_scan<kRadixThreads>(sum, s_warp, &total);
+#pragma unroll
+  for (int k = 0; k < DPT; ++k) {
+    goff[p * BINS + threadIdx.x * DPT + k] = run;
+    run += v[k];
+  }
 }
 
 __device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
@@ -157,29 +178,40 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
   return v;
 }
 
-template <int kWindow>
+// Shared memory of one pass (dynamic: 52 KB at 512 bins).
+template <int BINS>
+struct PassSmem {
+  uint32_t keys[kRadixTile];
+  uint32_t vals[kRadixTile];
+  uint32_t run[kRadixWarps][BINS];
+  uint32_t tile_excl[BINS];
+  uint32_t gbase[BINS];
+  uint32_t warp_scan[kRadixThreads / 32 + 1];
+  uint32_t tile;
+};
+
+template <int BINS, int kWindow>
 __global__ void __launch_bounds__(kRadixThreads, 3)
 onesweep_pass_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                      uint64_t n, int shift, int bits, const uint32_t* __restrict__ goff,
                      uint64_t* __restrict__ status, uint32_t* __restrict__ tile_counter,
                      uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
-  __shared__ uint32_t s_keys[kRadixTile];
-  __shared__ uint32_t s_vals[kRadixTile];
-  __shared__ uint32_t s_run[kRadixWarps][kRadixBins];
-  __shared__ uint32_t s_tile_excl[kRadixBins];
-  __shared__ uint32_t s_gbase[kRadixBins];
-  __shared__ uint32_t s_warp[kRadixThreads / 32 + 1];
-  __shared__ uint32_t s_tile;
+  constexpr int DPT = BINS / kRadixThreads;  // digits per thread (consecutive)
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  PassSmem<BINS>& sm = *reinterpret_cast<PassSmem<BINS>*>(smem_raw);
 
   const uint32_t mask = (1u << bits) - 1u;
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   // Dynamic tile ids in launch order: every predecessor of a tile was
   // scheduled before it, so the look-back below always makes progress.
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+  if (threadIdx.x == 0) sm.tile = atomicAdd(tile_counter, 1u);
 #pragma unroll
-  for (int w = 0; w < kRadixWarps; ++w) s_run[w][threadIdx.x] = 0;
+  for (int w = 0; w < kRadixWarps; ++w) {
+#pragma unroll
+    for (int k = 0; k < DPT; ++k) sm.run[w][threadIdx.x * DPT + k] = 0;
+  }
   __syncthreads();
-  const uint32_t tile = s_tile;
+  const uint32_t tile = sm.tile;
   const uint64_t tile_base = static_cast<uint64_t>(tile) * kRadixTile;
 
   uint32_t k[kRadixItems], v[kRadixItems], rank[kRadixItems];
@@ -197,90 +229,111 @@ onesweep_pass_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __res
     const bool valid = sub_base + static_cast<uint64_t>(r) * 32 + lane < n;
     const uint32_t d = (k[r] >> shift) & mask;
     if (warp_uniform(d, valid)) {
-      rank[r] = s_run[warp][d] + lane;
+      rank[r] = sm.run[warp][d] + lane;
       __syncwarp();
-      if (lane == 0) s_run[warp][d] += 32u;
+      if (lane == 0) sm.run[warp][d] += 32u;
     } else {
       const unsigned peers = digit_peers(d, valid, bits);
-      rank[r] = valid ? s_run[warp][d] + __popc(peers & lt) : 0u;
+      rank[r] = valid ? sm.run[warp][d] + __popc(peers & lt) : 0u;
       __syncwarp();
-      if (valid && (peers & lt) == 0) s_run[warp][d] += __popc(peers);
+      if (valid && (peers & lt) == 0) sm.run[warp][d] += __popc(peers);
     }
     __syncwarp();
   }
   __syncthreads();
 
-  // Per digit (thread = digit): tile count, warp prefix, look-back.
-  const uint32_t d = threadIdx.x;
-  uint32_t count = 0;
+  // Per digit (thread t: digits t*DPT ..): tile count, warp prefix, look-back.
+  uint32_t count[DPT], sum = 0;
 #pragma unroll
-  for (int w = 0; w < kRadixWarps; ++w) {
-    const uint32_t t = s_run[w][d];
-    s_run[w][d] = count;
-    count += t;
-  }
-  uint64_t* my = status + static_cast<uint64_t>(tile) * kRadixBins + d;
-  uint64_t excl = 0;
-  if (tile == 0) {
-    st_relaxed_u64(my, kFlagInc | count);
-  } else {
-    st_relaxed_u64(my, kFlagAgg | count);
-    // Windowed look-back: kWindow predecessor words in flight at once, then
-    // consumed nearest-first until an inclusive prefix is found; a
-    // not-yet-published word restarts the window at that tile.  Measured at
-    // C2 (4.2M pairs, 4 passes): window 1 / 2 / 4 / 8 / 16 / 32 ->
-    // 0.223 / 0.218 / 0.217 / 0.230 / 0.286 / 0.399 ms per sort (larger
-    // windows spill under the 3-blocks/SM register cap); default 4
-    // (TIERSHARD_LOOKBACK).
-    int64_t p = static_cast<int64_t>(tile) - 1;
-    bool done = false;
-    while (!done) {
-      uint64_t s[kWindow];
+  for (int q = 0; q < DPT; ++q) {
+    const uint32_t d = threadIdx.x * DPT + q;
+    uint32_t c = 0;
 #pragma unroll
-      for (int w = 0; w < kWindow; ++w) {
-        s[w] = p - w >= 0 ? ld_relaxed_u64(status + static_cast<uint64_t>(p - w) * kRadixBins + d)
-                          : kFlagInc;
-      }
-      int used = 0;
-#pragma unroll
-      for (int w = 0; w < kWindow; ++w) {
-        if (done || used != w) break;
-        const uint64_t flag = s[w] & ~kCountMask;
-        if (flag == 0) break;  // not ready: re-poll from here
-        excl += s[w] & kCountMask;
-        done = flag == kFlagInc;
-        ++used;
-      }
-      p -= used;
+    for (int w = 0; w < kRadixWarps; ++w) {
+      const uint32_t t = sm.run[w][d];
+      sm.run[w][d] = c;
+      c += t;
     }
-    st_relaxed_u64(my, kFlagInc | (excl + count));
+    count[q] = c;
+    sum += c;
+  }
+  uint64_t excl[DPT];
+#pragma unroll
+  for (int q = 0; q < DPT; ++q) {
+    const uint32_t d = threadIdx.x * DPT + q;
+    uint64_t* my = status + static_cast<uint64_t>(tile) * BINS + d;
+    excl[q] = 0;
+    if (tile == 0) {
+      st_relaxed_u64(my, kFlagInc | count[q]);
+    } else {
+      st_relaxed_u64(my, kFlagAgg | count[q]);
+    }
+  }
+  if (tile != 0) {
+#pragma unroll
+    for (int q = 0; q < DPT; ++q) {
+      const uint32_t d = threadIdx.x * DPT + q;
+      // Windowed look-back: kWindow predecessor words in flight at once, then
+      // consumed nearest-first until an inclusive prefix is found; a
+      // not-yet-published word restarts the window at that tile.  Measured
+      // at C2 (4.2M pairs, 4 x 8-bit passes): window 1 / 2 / 4 / 8 / 16 / 32
+      // -> 0.223 / 0.218 / 0.217 / 0.230 / 0.286 / 0.399 ms per sort
+      // (larger windows spill under the 3-blocks/SM register cap); default 4
+      // (TIERSHARD_LOOKBACK).
+      int64_t p = static_cast<int64_t>(tile) - 1;
+      bool done = false;
+      while (!done) {
+        uint64_t sw[kWindow];
+#pragma unroll
+        for (int w = 0; w < kWindow; ++w) {
+          sw[w] = p - w >= 0 ? ld_relaxed_u64(status + static_cast<uint64_t>(p - w) * BINS + d) : kFlagInc;
+        }
+        int used = 0;
+#pragma unroll
+        for (int w = 0; w < kWindow; ++w) {
+          if (done || used != w) break;
+          const uint64_t flag = sw[w] & ~kCountMask;
+          if (flag == 0) break;  // not ready: re-poll from here
+          excl[q] += sw[w] & kCountMask;
+          done = flag == kFlagInc;
+          ++used;
+        }
+        p -= used;
+      }
+      st_relaxed_u64(status + static_cast<uint64_t>(tile) * BINS + d, kFlagInc | (excl[q] + count[q]));
+    }
   }
   uint32_t total;
-  const uint32_t tile_excl = block_exclusive_scan<kRadixThreads>(count, s_warp, &total);
-  s_tile_excl[d] = tile_excl;
-  s_gbase[d] = goff[d] + static_cast<uint32_t>(excl);
+  uint32_t run = block_exclusive_scan<kRadixThreads>(sum, sm.warp_scan, &total);
 #pragma unroll
-  for (int w = 0; w < kRadixWarps; ++w) s_run[w][d] += tile_excl;
+  for (int q = 0; q < DPT; ++q) {
+    const uint32_t d = threadIdx.x * DPT + q;
+    sm.tile_excl[d] = run;
+    sm.gbase[d] = goff[d] + static_cast<uint32_t>(excl[q]);
+#pragma unroll
+    for (int w = 0; w < kRadixWarps; ++w) sm.run[w][d] += run;
+    run += count[q];
+  }
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kRadixItems; ++r) {
     const uint64_t i = sub_base + static_cast<uint64_t>(r) * 32 + lane;
     if (i < n) {
       const uint32_t dd = (k[r] >> shift) & mask;
-      const uint32_t pos = s_run[warp][dd] + rank[r];
-      s_keys[pos] = k[r];
-      s_vals[pos] = v[r];
+      const uint32_t pos = sm.run[warp][dd] + rank[r];
+      sm.keys[pos] = k[r];
+      sm.vals[pos] = v[r];
     }
   }
   __syncthreads();
   const uint64_t left = n - tile_base;
   const uint32_t tile_n = left < kRadixTile ? static_cast<uint32_t>(left) : kRadixTile;
   for (uint32_t j = threadIdx.x; j < tile_n; j += kRadixThreads) {
-    const uint32_t kk = s_keys[j];
+    const uint32_t kk = sm.keys[j];
     const uint32_t dd = (kk >> shift) & mask;
-    const uint32_t dst = s_gbase[dd] + (j - s_tile_excl[dd]);
+    const uint32_t dst = sm.gbase[dd] + (j - sm.tile_excl[dd]);
     keys_out[dst] = kk;
-    vals_out[dst] = s_vals[j];
+    vals_out[dst] = sm.vals[j];
   }
 }
 
@@ -377,6 +430,63 @@ void device_exclusive_scan(const uint32_t* in, uint32_t* out, uint64_t n, uint32
   TSD_LAUNCH_CHECK();
 }
 
+template <int BINS>
+void radix_sort_pairs_bins(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t n, int key_bits,
+                           const RadixBuffers& buf, uint32_t** keys_out, uint32_t** vals_out,
+                           cudaStream_t stream) {
+  constexpr int DIGIT_BITS = BINS == 512 ? 9 : 8;
+  const int passes = (key_bits + DIGIT_BITS - 1) / DIGIT_BITS;
+  const uint32_t tiles = static_cast<uint32_t>(radix_tiles(n));
+  TSD_CUDA(cudaMemsetAsync(buf.ghist, 0, sizeof(uint32_t) * kMaxRadixPasses * kMaxRadixBins, stream));
+  TSD_CUDA(cudaMemsetAsync(buf.counters, 0, sizeof(uint32_t) * kMaxRadixPasses, stream));
+  TSD_CUDA(cudaMemsetAsync(buf.status, 0, sizeof(uint64_t) * passes * tiles * BINS, stream));
+  onesweep_hist_kernel<BINS><<<tiles, kRadixThreads, 0, stream>>>(keys_in, n, key_bits, passes, buf.ghist);
+  TSD_LAUNCH_CHECK();
+  onesweep_offsets_kernel<BINS><<<passes, kRadixThreads, 0, stream>>>(buf.ghist, buf.goff);
+  TSD_LAUNCH_CHECK();
+  static const int window = [] {
+    const char* e = std::getenv("TIERSHARD_LOOKBACK");
+    return e ? std::atoi(e) : 4;
+  }();
+  const uint32_t* cur_k = keys_in;
+  const uint32_t* cur_v = vals_in;
+  for (int pass = 0; pass < passes; ++pass) {
+    const int shift = DIGIT_BITS * pass;
+    const int bits = key_bits - shift < DIGIT_BITS ? key_bits - shift : DIGIT_BITS;
+    uint32_t* out_k = (pass & 1) ? buf.keys_b : buf.keys_a;
+    uint32_t* out_v = (pass & 1) ? buf.vals_b : buf.vals_a;
+    const auto launch = [&](auto kern) {
+      static bool configured = false;  // per instantiation: opt in to > 48 KB of shared memory
+      if (!configured) {
+        TSD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(sizeof(PassSmem<BINS>))));
+        configured = true;
+      }
+      kern<<<tiles, kRadixThreads, sizeof(PassSmem<BINS>), stream>>>(
+          cur_k, cur_v, n, shift, bits, buf.goff + pass * BINS,
+          buf.status + static_cast<uint64_t>(pass) * tiles * BINS, buf.counters + pass, out_k, out_v);
+    };
+    if (window >= 8) launch(onesweep_pass_kernel<BINS, 8>);
+    else if (window >= 4) launch(onesweep_pass_kernel<BINS, 4>);
+    else if (window >= 2) launch(onesweep_pass_kernel<BINS, 2>);
+    else launch(onesweep_pass_kernel<BINS, 1>);
+    TSD_LAUNCH_CHECK();
+    cur_k = out_k;
+    cur_v = out_v;
+  }
+  *keys_out = const_cast<uint32_t*>(cur_k);
+  *vals_out = const_cast<uint32_t*>(cur_v);
+}
+
+int radix_digit_bits(int key_bits) {
+  static const bool allow9 = [] {
+    const char* e = std::getenv("TIERSHARD_RADIX9");
+    return !(e && std::string(e) == "0");
+  }();
+  // 9-bit digits only where they save a pass: 25..27 bits in 3 passes
+  return allow9 && key_bits > 24 && key_bits <= 27 ? 9 : 8;
+}
+
 void radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t n, int key_bits,
                       const RadixBuffers& buf, uint32_t** keys_out, uint32_t** vals_out,
                       cudaStream_t stream) {
@@ -387,43 +497,11 @@ void radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t
   if (n == 0) return;
   if (key_bits < 1) key_bits = 1;
   if (key_bits > 32) key_bits = 32;
-  const int passes = (key_bits + 7) / 8;
-  const uint32_t tiles = static_cast<uint32_t>(radix_tiles(n));
-  TSD_CUDA(cudaMemsetAsync(buf.ghist, 0, sizeof(uint32_t) * kMaxRadixPasses * kRadixBins, stream));
-  TSD_CUDA(cudaMemsetAsync(buf.counters, 0, sizeof(uint32_t) * kMaxRadixPasses, stream));
-  TSD_CUDA(cudaMemsetAsync(buf.status, 0, sizeof(uint64_t) * passes * tiles * kRadixBins, stream));
-  onesweep_hist_kernel<<<tiles, kRadixThreads, 0, stream>>>(keys_in, n, key_bits, passes, buf.ghist);
-  TSD_LAUNCH_CHECK();
-  onesweep_offsets_kernel<<<passes, kRadixThreads, 0, stream>>>(buf.ghist, buf.goff);
-  TSD_LAUNCH_CHECK();
-  const uint32_t* cur_k = keys_in;
-  const uint32_t* cur_v = vals_in;
-  for (int pass = 0; pass < passes; ++pass) {
-    const int shift = 8 * pass;
-    const int bits = key_bits - shift < 8 ? key_bits - shift : 8;
-    uint32_t* out_k = (pass & 1) ? buf.keys_b : buf.keys_a;
-    uint32_t* out_v = (pass & 1) ? buf.vals_b : buf.vals_a;
-    static const int window = [] {
-      const char* e = std::getenv("TIERSHARD_LOOKBACK");
-      return e ? std::atoi(e) : 4;
-    }();
-    const auto launch = [&](auto kern) {
-      kern<<<tiles, kRadixThreads, 0, stream>>>(cur_k, cur_v, n, shift, bits, buf.goff + pass * kRadixBins,
-                                                buf.status + static_cast<uint64_t>(pass) * tiles * kRadixBins,
-                                                buf.counters + pass, out_k, out_v);
-    };
-    if (window >= 32) launch(onesweep_pass_kernel<32>);
-    else if (window >= 16) launch(onesweep_pass_kernel<16>);
-    else if (window >= 8) launch(onesweep_pass_kernel<8>);
-    else if (window >= 4) launch(onesweep_pass_kernel<4>);
-    else if (window >= 2) launch(onesweep_pass_kernel<2>);
-    else launch(onesweep_pass_kernel<1>);
-    TSD_LAUNCH_CHECK();
-    cur_k = out_k;
-    cur_v = out_v;
+  if (radix_digit_bits(key_bits) == 9) {
+    radix_sort_pairs_bins<512>(keys_in, vals_in, n, key_bits, buf, keys_out, vals_out, stream);
+  } else {
+    radix_sort_pairs_bins<256>(keys_in, vals_in, n, key_bits, buf, keys_out, vals_out, stream);
   }
-  *keys_out = const_cast<uint32_t*>(cur_k);
-  *vals_out = const_cast<uint32_t*>(cur_v);
 }
 
 void segment_starts(const uint32_t* sorted_keys, uint64_t n, uint32_t* starts, uint32_t* seg_keys,

@@ -48,16 +48,19 @@ void device_exclusive_scan(const uint32_t* in, uint32_t* out, uint64_t n, uint32
                            uint32_t* d_total, cudaStream_t stream);
 
 constexpr int kMaxRadixPasses = 4;
+constexpr int kMaxRadixBins = 512;  // 9-bit digits when they save a pass
+// Digit width radix_sort_pairs uses for keys of `key_bits` bits (8 or 9).
+int radix_digit_bits(int key_bits);
 
 struct RadixBuffers {
   uint32_t* keys_a;    // n
   uint32_t* vals_a;    // n
   uint32_t* keys_b;    // n
   uint32_t* vals_b;    // n
-  uint32_t* ghist;     // kMaxRadixPasses * 256 digit totals
-  uint32_t* goff;      // kMaxRadixPasses * 256 exclusive digit offsets (goff[0..] of pass 0
-                       // are the bucket starts when a single pass sorts bucket ids)
-  uint64_t* status;    // kMaxRadixPasses * radix_tiles(n) * 256 look-back words
+  uint32_t* ghist;     // kMaxRadixPasses * kMaxRadixBins digit totals
+  uint32_t* goff;      // kMaxRadixPasses * kMaxRadixBins exclusive digit offsets (goff[0..]
+                       // of pass 0 are the bucket starts when one 8-bit pass sorts bucket ids)
+  uint64_t* status;    // kMaxRadixPasses * radix_tiles(n) * kMaxRadixBins look-back words
   uint32_t* counters;  // kMaxRadixPasses dynamic tile counters
 };
 

@@ -273,10 +273,10 @@ struct ts_table {
     keys_b.ensure(m);
     vals_b.ensure(m);
     const uint64_t tiles = tsd::radix_tiles(m);
-    ghist.ensure(tsd::kMaxRadixPasses * tsd::kRadixBins);
-    goff.ensure(tsd::kMaxRadixPasses * tsd::kRadixBins);
+    ghist.ensure(tsd::kMaxRadixPasses * tsd::kMaxRadixBins);
+    goff.ensure(tsd::kMaxRadixPasses * tsd::kMaxRadixBins);
     sort_counters.ensure(tsd::kMaxRadixPasses);
-    sort_status.ensure(tsd::kMaxRadixPasses * tiles * tsd::kRadixBins);
+    sort_status.ensure(tsd::kMaxRadixPasses * tiles * tsd::kMaxRadixBins);
     starts.ensure(m + 1);
     seg_keys.ensure(m + 1);
     seg_scratch.ensure(tsd::segment_scratch_elems(m) + 8);
