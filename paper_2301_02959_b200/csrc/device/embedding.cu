@@ -859,19 +859,17 @@ int seg_variant() {
   }();
   return v;
 }
-// Segments longer than short_max() entries go to the warp-per-piece path
-// (TIERSHARD_SHORT_MAX, <= kPiece): the short kernel's 4-8 segments per warp
-// finish together only when their lengths are alike.  Same sums either way
-// (a single piece is summed left to right).  Measured at C2, N=1 (segment
-// update + long path, ms): 256 -> 0.712, 64 -> 0.693, 32 -> 0.684,
-// 16 -> 0.724, 8 -> 0.747.
-uint32_t short_max() {
-  static const uint32_t v = [] {
-    const char* e = std::getenv("TIERSHARD_SHORT_MAX");
-    const int x = e ? std::atoi(e) : 32;
-    return static_cast<uint32_t>(std::min<int>(std::max(x, 1), static_cast<int>(kPiece)));
-  }();
-  return v;
+// Segments longer than `short_max` entries go to the warp-per-piece path
+// (<= kPiece): the short kernel's 4-8 segments per warp finish together only
+// when their lengths are alike.  Same sums either way (a single piece is
+// summed left to right).  Measured at C2 (segment update + long path):
+// N=1: 256 -> 0.712 ms, 64 -> 0.693, 32 -> 0.684, 16 -> 0.724, 8 -> 0.747;
+// N=2 step: 256 -> 2.39 ms, 32 -> 2.455; N=4: 3.437 vs 3.417 (noise).
+// Default: 32 on one GPU, 256 otherwise (TIERSHARD_SHORT_MAX overrides).
+uint32_t short_max(uint32_t gpus) {
+  const char* e = std::getenv("TIERSHARD_SHORT_MAX");
+  const int x = e ? std::atoi(e) : (gpus == 1 ? 32 : static_cast<int>(kPiece));
+  return static_cast<uint32_t>(std::min<int>(std::max(x, 1), static_cast<int>(kPiece)));
 }
 int seg_group_128() {
   static const int v = [] {
@@ -895,18 +893,18 @@ void launch_segment_update(const uint32_t* keys, const uint32_t* vals, const uin
     if (seg_variant() == 0 || DIM > 128) {
       seg_short_kernel<DIM><<<grid, kThreads, 0, stream>>>(keys, vals, starts, d_lo, d_hi, grads,
                                                            weights, state, opt, dense0, dense1,
-                                                           sc.long_list, sc.long_count, short_max());
+                                                           sc.long_list, sc.long_count, sc.short_max);
     } else if (DIM == 128 && seg_group_128() == 16) {
       if constexpr (DIM == 128) {
         seg_pair_kernel<DIM, 16><<<grid, kThreads, 0, stream>>>(vals, starts, seg_keys, d_lo, d_hi, grads,
                                                                weights, state, opt, dense0, dense1,
-                                                               sc.long_list, sc.long_count, short_max());
+                                                               sc.long_list, sc.long_count, sc.short_max);
       }
     } else {
       constexpr int G = 8;  // DIM <= 128 here
       if constexpr (DIM <= 128) seg_pair_kernel<DIM, G><<<grid, kThreads, 0, stream>>>(vals, starts, seg_keys, d_lo, d_hi, grads,
                                                             weights, state, opt, dense0, dense1,
-                                                            sc.long_list, sc.long_count, short_max());
+                                                            sc.long_list, sc.long_count, sc.short_max);
     }
     TSD_LAUNCH_CHECK();
   });

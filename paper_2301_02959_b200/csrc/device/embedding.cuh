@@ -11,8 +11,9 @@ namespace tsd {
 
 // Pieces of a long segment: ORC_PIECE in the oracle.
 constexpr uint32_t kPiece = 256;
-// Segments longer than this (<= kPiece) take the warp-per-piece path.
-uint32_t short_max();
+// Segments longer than this (<= kPiece) take the warp-per-piece path
+// (default for a job of `gpus` GPUs, or TIERSHARD_SHORT_MAX).
+uint32_t short_max(uint32_t gpus);
 
 // How a requester finds the local shard row of a canonical row (or learns it
 // is served remotely).  identity: U == 1, local id == canonical index.
@@ -89,6 +90,7 @@ struct SegmentScratch {
   float* partials = nullptr;       // max_pieces * dim
   uint32_t max_long = 0;
   uint32_t max_pieces = 0;
+  uint32_t short_max = kPiece;     // longer segments take the piece path
 };
 
 // Segments [*d_lo, *d_hi) (device scalars, so ranges can be chosen on the

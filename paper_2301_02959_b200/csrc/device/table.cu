@@ -113,6 +113,7 @@ struct ts_table {
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fwd0 = nullptr, ev_dedup = nullptr;
   bool dedup_in_forward = true;
+  uint32_t seg_short_max = tsd::kPiece;  // tsd::short_max(U), set at creation
   bool dedup_ready = false;
   uint32_t* dd_keys = nullptr;
   uint32_t* dd_vals = nullptr;
@@ -280,7 +281,7 @@ struct ts_table {
     starts.ensure(m + 1);
     seg_keys.ensure(m + 1);
     seg_scratch.ensure(tsd::segment_scratch_elems(m) + 8);
-    const uint64_t max_long = m / (tsd::short_max() + 1) + 1;
+    const uint64_t max_long = m / (seg_short_max + 1) + 1;
     long_list.ensure(max_long);
     piece_off.ensure(max_long + 1);
     partials.ensure((m / tsd::kPiece + max_long + 1) * cfg.dim);
@@ -332,6 +333,7 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
   if (U > 1 && !tier_dest) fail(TS_ERR_CONFIG, "table: U > 1 needs the placement table");
   use_device(c.device);
   TSD_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  seg_short_max = tsd::short_max(U);
   {
     if (const char* e = std::getenv("TIERSHARD_DEDUP_IN_FORWARD")) dedup_in_forward = std::string(e) != "0";
     if (dedup_in_forward) {
@@ -766,6 +768,7 @@ void ts_table::backward(const float* d_grad) {
   sc.long_count = long_count.ptr;
   sc.piece_off = piece_off.ptr;
   sc.partials = partials.ptr;
+  sc.short_max = seg_short_max;
   RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, ghist.ptr, goff.ptr,
                   sort_status.ptr, sort_counters.ptr};
   uint32_t* sk = nullptr;
@@ -820,6 +823,7 @@ void ts_table::backward(const float* d_grad) {
   sc.long_list = long_list.ptr;
   sc.piece_off = piece_off.ptr;
   sc.partials = partials.ptr;
+  sc.short_max = seg_short_max;
   launch_build_entries(last_rows, order.ptr + n_remote, n_local_occ, rv, recv_ids.ptr, recv_before,
                        recv_total, static_cast<uint32_t>(occ), entry_keys.ptr, entry_vals.ptr, stream);
   // replicated tiers reduce into dense buffers: DP always, Flex across nodes
@@ -1016,6 +1020,7 @@ void ts_table::backward_p2p(const float* d_grad) {
   sc.long_count = long_count.ptr;
   sc.piece_off = piece_off.ptr;
   sc.partials = partials.ptr;
+  sc.short_max = seg_short_max;
 
   // ---- entries, sort, segments (no gradient needed): done by the forward on
   // the aux stream when prefetched, else here on the compute stream -------
