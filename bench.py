@@ -273,6 +273,8 @@ def run_ours(args, dist: Dist):
     n_gpus = dist.world if dist.world > 1 else args.gpus
     if dist.world == 1 and n_gpus > 1:
         raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    if ts.device_count() == 0:  # the product path has no CPU fallback: fail before preparing anything
+        raise SystemExit("tiershard-b200: NoDevice: no CUDA device available (no CPU fallback)")
     spec, data_dir, doc = prepare(args, dist, n_gpus)
     exp = doc["export"]
     u, w = exp["num_gpus"], exp["gpus_per_node"]
