@@ -404,6 +404,15 @@ def run_ours(args, dist: Dist):
                "per_call_value": samples / e2e_call_s,
                "per_call_step_wall_ms": [round(float(np.percentile(step_wall, q)), 3) for q in (0, 50, 100)]}
         if os.environ.get("TS_BENCH_DIAG"):
+            # diagnostic: the device-resident steps timed by wall clock, no L2
+            # flush (the apples-to-apples partner of the e2e wall time)
+            torch.cuda.synchronize()
+            dist.barrier()
+            t1 = time.perf_counter()
+            for k in range(args.steps):
+                step(k)
+            table.synchronize()
+            e2e["diag_device_wall_value"] = samples / dist.max(time.perf_counter() - t1)
             # diagnostic variant: same host copies, torch-owned device buffers
             pin_t = [torch.from_numpy(b.view(np.int32)).pin_memory() for b in batches]
             dist.barrier()
