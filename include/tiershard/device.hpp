@@ -112,6 +112,24 @@ class DeviceSampler {
   ts_sampler* sampler_ = nullptr;
 };
 
+// GPU planner preview for what-if sweeps (tiershard_b200.h
+// ts_frontier_preview): landmarks, 2- and 3-tier cuts and predicted
+// reductions for every (cost model, topology) pair over one distribution.
+// The host planner (plan_2tier / plan_3tier) stays authoritative; a preview
+// cut can differ from it by a row.
+struct PlanPreview {
+  FrontierLandmarks landmarks;
+  uint64_t dp_cut_2tier = 0;
+  uint64_t dp_cut_3tier = 0, flex_cut_3tier = 0;
+  double reduction_2tier = 0.0, reduction_3tier = 0.0;
+};
+struct WhatIf {
+  CostModelConfig cost_model;
+  Topology topology;
+};
+std::vector<PlanPreview> preview_plans(const RowDistribution& dist, const std::vector<WhatIf>& what_if,
+                                       int device = 0);
+
 // One rank's shard of the tiered table.  Collective when N*W > 1.
 class SequenceEmbedding {
  public:

@@ -166,6 +166,34 @@ ts_status ts_sampler_iteration(ts_sampler* s, uint32_t iteration, uint64_t sampl
 ts_status ts_sampler_destroy(ts_sampler* s);
 
 /* ------------------------------------------------------------------------
+ * Planner preview: frontier landmarks and 2- / 3-tier
+ * cuts for many what-if cost models over one canonical distribution, from
+ * one GPU prefix scan (planner.cpp build_frontier / find_points /
+ * plan_2tier / plan_3tier restated on mem(k) = k*mem_a + mem_b*P(k)).  The
+ * host planner stays authoritative: the scan's summation order can move a
+ * cut by a row where the frontier crosses zero within rounding.
+ * ---------------------------------------------------------------------- */
+typedef struct ts_frontier_query {
+  double mem_a;        /* DP memory marginal of a row: mem_a + mem_b * p (bytes) */
+  double mem_b;
+  double p_comm_dp;    /* DP communication breakpoint (landmark c) */
+  double flex_price;   /* Flex memory price per row (3-tier) */
+  double p_comm_flex;  /* Flex communication breakpoint; < 0: no Flex tier (2-tier only) */
+} ts_frontier_query;
+
+typedef struct ts_frontier_answer {
+  uint64_t a, b, c;          /* find_points landmarks (d = n) */
+  uint64_t dp_cut_3tier;     /* 3-tier cuts (== b, b without a Flex tier) */
+  uint64_t flex_cut_3tier;
+  double reduction_2tier;    /* predicted global-a2a reduction = covered expected length share */
+  double reduction_3tier;
+} ts_frontier_answer;
+
+/* probabilities: n canonical (non-increasing) probabilities, host memory. */
+ts_status ts_frontier_preview(int device, uint64_t n, const double* probabilities, uint32_t nq,
+                              const ts_frontier_query* queries, ts_frontier_answer* answers);
+
+/* ------------------------------------------------------------------------
  * Host-only planning helpers of the U > 1 path (no device needed).
  * ---------------------------------------------------------------------- */
 

@@ -76,6 +76,7 @@ EXPORTS = (
     "ts_sampler_iteration",
     "ts_sampler_destroy",
     "ts_table_train_steps_host",
+    "ts_frontier_preview",
 )
 
 
@@ -166,6 +167,7 @@ def load() -> C.CDLL:
         "ts_sampler_iteration": (C.c_int, [vp, C.c_uint32, C.c_uint64, C.c_uint32, vp, C.c_uint64, vp, u64p, vp]),
         "ts_sampler_destroy": (C.c_int, [vp]),
         "ts_table_train_steps_host": (C.c_int, [vp, vp, vp, C.c_uint32, vp]),
+        "ts_frontier_preview": (C.c_int, [C.c_int, C.c_uint64, vp, C.c_uint32, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -5,6 +5,7 @@
 
 #include "capi_check.hpp"
 #include "parallel.hpp"
+#include "tiershard/cost_model.hpp"
 #include "tiershard/error.hpp"
 #include "tiershard/rng.hpp"
 #include "tiershard/simulator.hpp"
@@ -120,6 +121,46 @@ uint64_t DeviceSampler::sample(uint32_t iteration, uint64_t sample_begin, uint32
   detail::check(ts_sampler_iteration(sampler_, iteration, sample_begin, samples, d_rows, capacity, d_offsets,
                                      &occ, stream));
   return occ;
+}
+
+std::vector<PlanPreview> preview_plans(const RowDistribution& dist, const std::vector<WhatIf>& what_if,
+                                       int device) {
+  if (dist.rows().empty()) throw ValidationError("frontier: distribution has no materialized rows");
+  if (!dist.is_sorted()) throw ValidationError("frontier: distribution is not in canonical order");
+  std::vector<ts_frontier_query> q(what_if.size());
+  for (size_t i = 0; i < what_if.size(); ++i) {
+    const CostModelConfig& cfg = what_if[i].cost_model;
+    const Topology& topo = what_if[i].topology;
+    cfg.validate();
+    topo.validate();
+    // the DP memory marginal is affine in p (table_cost differenced)
+    const double m0 = marginal_cost_dp(0.0, cfg, topo).memory_bytes;
+    const double m1 = marginal_cost_dp(1.0, cfg, topo).memory_bytes;
+    const Breakpoints bp = find_breakpoints(cfg, topo);
+    q[i].mem_a = m0;
+    q[i].mem_b = m1 - m0;
+    q[i].p_comm_dp = bp.p_comm_dp;
+    q[i].flex_price = bp.flex_mem_price_bytes;
+    q[i].p_comm_flex = topo.has_fast_intra_tier() && bp.p_comm_flex ? *bp.p_comm_flex : -1.0;
+  }
+  std::vector<double> p(dist.rows().size());
+  for (size_t i = 0; i < p.size(); ++i) p[i] = dist.rows()[i].probability;
+  std::vector<ts_frontier_answer> a(q.size());
+  detail::check(ts_frontier_preview(device, p.size(), p.data(), static_cast<uint32_t>(q.size()), q.data(),
+                                    a.data()));
+  std::vector<PlanPreview> out(q.size());
+  for (size_t i = 0; i < q.size(); ++i) {
+    out[i].landmarks.a = a[i].a;
+    out[i].landmarks.b = a[i].b;
+    out[i].landmarks.c = a[i].c;
+    out[i].landmarks.d = p.size();
+    out[i].dp_cut_2tier = a[i].b;
+    out[i].dp_cut_3tier = a[i].dp_cut_3tier;
+    out[i].flex_cut_3tier = a[i].flex_cut_3tier;
+    out[i].reduction_2tier = a[i].reduction_2tier;
+    out[i].reduction_3tier = a[i].reduction_3tier;
+  }
+  return out;
 }
 
 void SequenceEmbedding::backward(const float* d_grad) { detail::check(ts_table_backward(table_, d_grad)); }

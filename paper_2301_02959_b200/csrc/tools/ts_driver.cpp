@@ -19,6 +19,7 @@
 
 #include "json.hpp"
 #include "tiershard/cost_model.hpp"
+#include "tiershard/device.hpp"
 #include "tiershard/distribution.hpp"
 #include "tiershard/error.hpp"
 #include "tiershard/hashing.hpp"
@@ -300,6 +301,36 @@ Json run(const Json& spec) {
   const uint64_t hash_seed = spec.value("hash_seed", ts::kDefaultPlacementSeed);
   const auto placements = ts::assign_rows(plan, d, topo, hash_seed);
   out["placements_digest"] = digest_placements(placements);
+
+  if (spec.contains("preview")) {
+    // GPU planner preview of this spec's (cost model, topology) plus any
+    // what-if overrides, beside the authoritative host plans of each
+    std::vector<ts::WhatIf> wi{{cfg, topo}};
+    for (const Json& o : spec["preview"].value("what_if", Json::array())) {
+      wi.push_back({o.contains("cost_model") ? parse_cfg(o["cost_model"]) : cfg,
+                    o.contains("topology") ? parse_topology(o["topology"]) : topo});
+    }
+    t0 = seconds_now();
+    const std::vector<ts::PlanPreview> pv = ts::preview_plans(d, wi);
+    timing["preview_s"] = seconds_now() - t0;
+    Json arr = Json::array();
+    for (size_t i = 0; i < pv.size(); ++i) {
+      const ts::ShardingPlan p2 = ts::plan_2tier(d, wi[i].cost_model, wi[i].topology);
+      const ts::ShardingPlan p3 = ts::plan_3tier(d, wi[i].cost_model, wi[i].topology);
+      const ts::Frontier fr = ts::build_frontier(d, wi[i].cost_model, wi[i].topology, ts::Strategy::kDataParallel);
+      const ts::FrontierLandmarks lm = ts::find_points(fr, d, wi[i].cost_model, wi[i].topology);
+      arr.push_back({{"gpu", {{"a", pv[i].landmarks.a}, {"b", pv[i].landmarks.b}, {"c", pv[i].landmarks.c},
+                              {"dp_cut_2tier", pv[i].dp_cut_2tier}, {"dp_cut_3tier", pv[i].dp_cut_3tier},
+                              {"flex_cut_3tier", pv[i].flex_cut_3tier},
+                              {"reduction_2tier", pv[i].reduction_2tier},
+                              {"reduction_3tier", pv[i].reduction_3tier}}},
+                     {"host", {{"a", lm.a}, {"b", lm.b}, {"c", lm.c}, {"dp_cut_2tier", p2.dp_cut},
+                               {"dp_cut_3tier", p3.dp_cut}, {"flex_cut_3tier", p3.flex_cut},
+                               {"reduction_2tier", p2.predicted.global_a2a_reduction},
+                               {"reduction_3tier", p3.predicted.global_a2a_reduction}}}});
+    }
+    out["preview"] = arr;
+  }
 
   if (spec.contains("export_dir")) {
     // Bench/test preparation: the device remap bytes the planner emits, the
