@@ -1375,12 +1375,13 @@ ts_status ts_table_train_steps_host(ts_table* t, const uint32_t* const* h_rows, 
         TSD_CUDA(cudaEventRecord(t->ev_consumed[b], t->stream));
       }
     }
-    if (steps > t->h_loss_cap) {
+    if (steps > t->h_loss_cap) {  // pinning synchronises the device: grow rarely
       if (t->h_loss_pinned) TSD_CUDA(cudaFreeHost(t->h_loss_pinned));
       t->h_loss_pinned = nullptr;
       t->h_loss_cap = 0;
-      TSD_CUDA(cudaHostAlloc(&t->h_loss_pinned, sizeof(double) * steps, cudaHostAllocDefault));
-      t->h_loss_cap = steps;
+      const uint32_t cap = std::max<uint32_t>(steps, 4096);
+      TSD_CUDA(cudaHostAlloc(&t->h_loss_pinned, sizeof(double) * cap, cudaHostAllocDefault));
+      t->h_loss_cap = cap;
     }
     uint32_t* buf[2] = {t->rows_dev.ptr, t->rows_dev2.ptr};
     // step s's ids go to buffer s % 2 on the copy stream once step s-2 (the
