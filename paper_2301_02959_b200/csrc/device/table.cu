@@ -177,6 +177,7 @@ struct ts_table {
   std::vector<const float*> peer_grad;              // peers' gradient buffers (mapped)
   std::vector<float*> peer_dense_dp, peer_dense_flex;  // peers' partial receive buffers (mapped)
   std::vector<uint32_t*> peer_stamp_dp, peer_stamp_flex;  // and their slot stamps
+  std::vector<float*> peer_recv_rows;  // peers' gradient receive buffers (fixed: mapped once)
   uint32_t per_dp = 0, per_flex = 0;  // replicated rows owned per group member
   std::vector<float*> peer_w, peer_state;           // peers' shards (mapped)
   tsd::IpcExport my_export{};                       // staging for the step payload
@@ -522,11 +523,12 @@ void ts_table::setup_p2p() {
     std::memset(&e, 0, sizeof(e));
     return p ? export_pointer(p) : e;
   };
-  constexpr int kExports = 9;
+  constexpr int kExports = 10;
   IpcExport mine[kExports] = {export_pointer(send_ids.ptr), export_pointer(order.ptr),
                               export_pointer(loss_partials.ptr + gather_grid), exp_or_none(dense_dp.ptr),
                               export_pointer(d_w), exp_or_none(d_state), exp_or_none(dense_flex.ptr),
-                              exp_or_none(stamp_dp.ptr), exp_or_none(stamp_flex.ptr)};
+                              exp_or_none(stamp_dp.ptr), exp_or_none(stamp_flex.ptr),
+                              export_pointer(recv_rows.ptr)};
   const std::vector<uint8_t> all = allgather_bytes(mine, sizeof(mine));
   peer_ids.assign(U, nullptr);
   peer_pos.assign(U, nullptr);
@@ -539,6 +541,7 @@ void ts_table::setup_p2p() {
   peer_dense_flex[g] = dense_flex.ptr;
   peer_stamp_dp.assign(U, nullptr);
   peer_stamp_flex.assign(U, nullptr);
+  peer_recv_rows.assign(U, nullptr);
   peer_stamp_dp[g] = stamp_dp.ptr;
   peer_stamp_flex[g] = stamp_flex.ptr;
   for (uint32_t p = 0; p < U; ++p) {
@@ -556,6 +559,7 @@ void ts_table::setup_p2p() {
     peer_dense_flex[p] = static_cast<float*>(open_opt(e[6]));
     peer_stamp_dp[p] = static_cast<uint32_t*>(open_opt(e[7]));
     peer_stamp_flex[p] = static_cast<uint32_t*>(open_opt(e[8]));
+    peer_recv_rows[p] = static_cast<float*>(peers.open(pp, e[9]));
   }
   peer_grad.assign(U, nullptr);
   xfer.ensure(step_payload_bytes() * U);
@@ -1067,15 +1071,14 @@ void ts_table::backward_p2p(const float* d_grad) {
     TSD_CUDA(cudaStreamWaitEvent(comm, ev_bwd0, 0));
     int tx = phase_begin(kPhaseExchangeBwd, xs);
     if (recv_total * cfg.dim > recv_rows.cap) fail(TS_ERR_INTERNAL, "table: receive buffer overflow");
-    const IpcExport mine = export_pointer(grads_push ? static_cast<const void*>(recv_rows.ptr) : d_grad);
-    const std::vector<uint8_t> all = allgather_bytes(&mine, sizeof(mine));
     if (grads_push) {
+      // the receive buffers never move (mapped at setup), and the forward's
+      // all-gather already ordered every server's previous reads of them
+      // before this step: no rendezvous, no host sync before the push
       PushTable pt{};
       for (uint32_t p = 0; p < U; ++p) {
         if (p == g) continue;
-        IpcExport e;
-        std::memcpy(&e, all.data() + sizeof(e) * p, sizeof(e));
-        float* server_recv = static_cast<float*>(peers.open(static_cast<int>(p), e));
+        float* server_recv = peer_recv_rows[p];
         ExchangePlan sp;  // server p's receive layout: which slots hold our entries
         exchange_plan(N, W, p, h_counts.data(), &sp);
         for (int part = 0; part < 2; ++part) {
@@ -1093,6 +1096,8 @@ void ts_table::backward_p2p(const float* d_grad) {
       }
       barrier_on_comm();  // every requester's rows have landed in every server
     } else {
+      const IpcExport mine = export_pointer(d_grad);
+      const std::vector<uint8_t> all = allgather_bytes(&mine, sizeof(mine));
       PullGrads pg{};
       for (uint32_t p = 0; p < U; ++p) {
         if (p == g) continue;

@@ -47,6 +47,18 @@ def free_port():
     return p
 
 
+def run_ranks(u, worker_args, env=None):
+    """torchrun u ranks of mg_worker.py; a fresh port on a rendezvous-port race."""
+    for _ in range(3):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={u}",
+               "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+               str(ROOT / "tests" / "mg_worker.py"), *worker_args]
+        proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+        if proc.returncode == 0 or "EADDRINUSE" not in proc.stderr:
+            return proc
+    return proc
+
+
 CASES = [(1, 2, 1, "p2p"), (2, 1, 1, "p2p"), (2, 1, 0, "p2p"), (2, 2, 1, "p2p"), (1, 4, 1, "p2p"),
          (1, 2, 1, "p2p_pull"), (2, 2, 1, "p2p_pull"), (1, 4, 0, "p2p_pull"),
          (1, 2, 1, "nccl"), (2, 2, 1, "nccl"), (2, 1, 0, "nccl")]
@@ -61,13 +73,10 @@ def test_multi_gpu_matches_oracle(cuda, tmp_path, n_nodes, w, opt, exchange):
     u = n_nodes * w
     if n_devices() < u:
         pytest.skip(f"needs {u} GPUs")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={u}",
-           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
-           str(ROOT / "tests" / "mg_worker.py"), "--nodes", str(n_nodes), "--gpus-per-node", str(w),
-           "--optimizer", str(opt), "--lr", str(LR), "--out", str(tmp_path)]
     env = dict(os.environ, TIERSHARD_EXCHANGE="nccl" if exchange == "nccl" else "p2p",
                TIERSHARD_GRADS="pull" if exchange == "p2p_pull" else "push")
-    proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    proc = run_ranks(u, ["--nodes", str(n_nodes), "--gpus-per-node", str(w), "--optimizer", str(opt),
+                         "--lr", str(LR), "--out", str(tmp_path)], env)
     assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
     pb = mg_worker.problem(n_nodes, w)
     res = [np.load(tmp_path / f"rank{g}.npz") for g in range(u)]
@@ -117,13 +126,9 @@ def test_multi_gpu_host_steps_match_oracle(cuda, tmp_path, n_nodes, w, opt, pipe
     if n_devices() < u:
         pytest.skip(f"needs {u} GPUs")
     steps = 3
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={u}",
-           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
-           str(ROOT / "tests" / "mg_worker.py"), "--nodes", str(n_nodes), "--gpus-per-node", str(w),
-           "--optimizer", str(opt), "--lr", str(LR_STEPS), "--steps", str(steps), "--out", str(tmp_path)]
-    if pipelined:
-        cmd.append("--pipelined")
-    proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    args = ["--nodes", str(n_nodes), "--gpus-per-node", str(w), "--optimizer", str(opt), "--lr", str(LR_STEPS),
+            "--steps", str(steps), "--out", str(tmp_path)] + (["--pipelined"] if pipelined else [])
+    proc = run_ranks(u, args)
     assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
     pb = mg_worker.problem(n_nodes, w, steps=steps)
     res = [np.load(tmp_path / f"rank{g}.npz") for g in range(u)]
