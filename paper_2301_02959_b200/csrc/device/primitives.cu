@@ -456,11 +456,15 @@ void radix_sort_pairs_bins(const uint32_t* keys_in, const uint32_t* vals_in, uin
     uint32_t* out_k = (pass & 1) ? buf.keys_b : buf.keys_a;
     uint32_t* out_v = (pass & 1) ? buf.vals_b : buf.vals_a;
     const auto launch = [&](auto kern) {
-      static bool configured = false;  // per instantiation: opt in to > 48 KB of shared memory
-      if (!configured) {
+      // opt in to > 48 KB of shared memory, once per instantiation and device
+      static std::atomic<uint64_t> configured{0};
+      int dev = 0;
+      TSD_CUDA(cudaGetDevice(&dev));
+      const uint64_t bit = uint64_t{1} << (dev & 63);
+      if (!(configured.load(std::memory_order_relaxed) & bit)) {
         TSD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(sizeof(PassSmem<BINS>))));
-        configured = true;
+        configured.fetch_or(bit, std::memory_order_relaxed);
       }
       kern<<<tiles, kRadixThreads, sizeof(PassSmem<BINS>), stream>>>(
           cur_k, cur_v, n, shift, bits, buf.goff + pass * BINS,
