@@ -1,5 +1,9 @@
 // Device-wide scan, stable LSD radix sort and segment-start compaction
 // (declarations and design notes in primitives.cuh).
+#include <atomic>
+#include <cstdlib>
+#include <string>
+
 #include "common.cuh"
 #include "primitives.cuh"
 
