@@ -774,7 +774,11 @@ unsigned persistent_grid(unsigned per_sm) { return static_cast<unsigned>(sm_coun
 // lowers it so the exchange / replica kernels on the (high-priority) comm
 // stream always find free SM slots instead of queueing behind grids that
 // never retire a block (one table per process, set at creation).
-unsigned g_compute_blocks_per_sm = 8;
+// blocks per SM of the persistent compute grids (TIERSHARD_COMPUTE_BLOCKS)
+unsigned g_compute_blocks_per_sm = [] {
+  const char* e = std::getenv("TIERSHARD_COMPUTE_BLOCKS");
+  return e ? static_cast<unsigned>(std::max(1, std::atoi(e))) : 8u;
+}();
 
 }  // namespace
 
