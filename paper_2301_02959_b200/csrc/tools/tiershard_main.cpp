@@ -17,6 +17,10 @@
 //       predicted vs simulated metrics (compare, 2 % tolerance) on stdout.
 //   tiershard breakpoints --manifest M
 //       Breakpoints of the manifest's cost model and topology (JSON, stdout).
+//   tiershard preview     --manifest M [--plan SWEEP.json]
+//       GPU planner preview (device.hpp preview_plans) for the manifest's
+//       configuration and every what-if of SWEEP.json (a list of
+//       {"cost_model": {...}, "topology": {...}} overrides); JSON on stdout.
 //
 // DIR defaults to the manifest's output_dir (relative to the manifest).  The
 // plan of simulate/compare is P, else DIR/plan.json, else planned in
@@ -31,6 +35,7 @@
 #include <memory>
 #include <string>
 
+#include "tiershard/device.hpp"
 #include "tiershard/error.hpp"
 #include "tiershard/json_io.hpp"
 #include "tiershard/manifest.hpp"
@@ -52,7 +57,7 @@ struct Args {
 [[noreturn]] void usage(const char* msg) {
   std::fprintf(stderr,
                "tiershard %s: %s\n"
-               "usage: tiershard {synth|plan|simulate|compare|breakpoints} --manifest PATH "
+               "usage: tiershard {synth|plan|simulate|compare|breakpoints|preview} --manifest PATH "
                "[--out DIR] [--plan PATH] [--threads N]\n",
                std::string(ts::kVersion).c_str(), msg);
   std::exit(2);
@@ -215,6 +220,62 @@ int cmd_simulate(const Args& a, bool compare_only) {
   return 0;
 }
 
+// GPU planner preview over a what-if sweep: --plan names a JSON list of
+// {"cost_model": {...}, "topology": {...}} overrides of the manifest's
+// (either key optional); the manifest's own configuration comes first.
+int cmd_preview(const Args& a) {
+  const ts::Manifest m = ts::load_manifest(a.manifest);
+  const ts::Topology topo = ts::manifest_topology(m);
+  const ts::RowDistribution d = ts::build_merged_distribution(m);
+  std::vector<ts::WhatIf> wi{{m.cost_model, topo}};
+  if (!a.plan.empty()) {
+    std::ifstream in(a.plan);
+    if (!in) throw ts::ConfigError("preview: cannot open '" + a.plan.string() + "'");
+    nlohmann::json sweep;
+    try {
+      sweep = nlohmann::json::parse(in);
+    } catch (const nlohmann::json::parse_error& e) {
+      throw ts::ConfigError(std::string("preview: invalid JSON: ") + e.what());
+    }
+    for (const nlohmann::json& o : sweep) {
+      ts::WhatIf w{m.cost_model, topo};
+      if (o.contains("cost_model")) {
+        const nlohmann::json& c = o["cost_model"];
+        if (c.contains("local_batch")) w.cost_model.local_batch = c["local_batch"].get<uint32_t>();
+        if (c.contains("embedding_dim")) w.cost_model.embedding_dim = c["embedding_dim"].get<uint32_t>();
+        if (c.contains("scalar_bytes")) w.cost_model.scalar_bytes = c["scalar_bytes"].get<uint32_t>();
+        if (c.contains("dp_replication_multiplier")) {
+          w.cost_model.dp_replication_multiplier = c["dp_replication_multiplier"].get<double>();
+        }
+      }
+      if (o.contains("topology")) {
+        const nlohmann::json& t = o["topology"];
+        w.topology.num_nodes = t.value("num_nodes", w.topology.num_nodes);
+        w.topology.gpus_per_node = t.value("gpus_per_node", w.topology.gpus_per_node);
+        if (t.contains("a2a_global_gibs")) w.topology.a2a_global = t["a2a_global_gibs"].get<double>() * ts::kGiB;
+        if (t.contains("a2a_intra_gibs")) w.topology.a2a_intra = t["a2a_intra_gibs"].get<double>() * ts::kGiB;
+        if (t.contains("ar_global_gibs")) w.topology.ar_global = t["ar_global_gibs"].get<double>() * ts::kGiB;
+        if (t.contains("ar_cross_gibs")) w.topology.ar_cross = t["ar_cross_gibs"].get<double>() * ts::kGiB;
+      }
+      wi.push_back(w);
+    }
+  }
+  const std::vector<ts::PlanPreview> pv = ts::preview_plans(d, wi);
+  nlohmann::json out = nlohmann::json::array();
+  for (size_t i = 0; i < pv.size(); ++i) {
+    out.push_back({{"cost_model", ts::to_json(wi[i].cost_model)},
+                   {"topology", ts::to_json(wi[i].topology)},
+                   {"landmarks", {{"a", pv[i].landmarks.a}, {"b", pv[i].landmarks.b}, {"c", pv[i].landmarks.c},
+                                  {"d", pv[i].landmarks.d}}},
+                   {"plan_2tier", {{"dp_cut", pv[i].dp_cut_2tier},
+                                   {"global_a2a_reduction", pv[i].reduction_2tier}}},
+                   {"plan_3tier", {{"dp_cut", pv[i].dp_cut_3tier}, {"flex_cut", pv[i].flex_cut_3tier},
+                                   {"global_a2a_reduction", pv[i].reduction_3tier}}}});
+  }
+  std::cout << out.dump(2) << "\n";
+  return 0;
+}
+
 int cmd_breakpoints(const Args& a) {
   const ts::Manifest m = ts::load_manifest(a.manifest);
   const ts::Topology topo = ts::manifest_topology(m);
@@ -232,6 +293,7 @@ int main(int argc, char** argv) {
     if (a.command == "simulate") return cmd_simulate(a, false);
     if (a.command == "compare") return cmd_simulate(a, true);
     if (a.command == "breakpoints") return cmd_breakpoints(a);
+    if (a.command == "preview") return cmd_preview(a);
     usage(("unknown command " + a.command).c_str());
   } catch (const ts::ValidationError& e) {
     std::fprintf(stderr, "tiershard: ValidationError: %s\n", e.what());

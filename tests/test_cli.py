@@ -123,3 +123,31 @@ def test_simulate_matches_reference(name, tmp_path, cuda):
     assert "reduction" in p.stdout
     c = cli("compare", "--manifest", manifest, "--out", tmp_path / "out")
     assert c.returncode == 0 and "global_a2a" in c.stdout
+
+
+def test_preview_fails_loudly_without_device(tmp_path):
+    import paper_2301_02959_b200 as ts
+    if ts.device_count() > 0:
+        pytest.skip("a device is present")
+    manifest = io.write_case(tmp_path / "in", *io.CASES["zipf_2tier_1x8"], sim=False)
+    p = cli("preview", "--manifest", manifest)
+    assert p.returncode == 3 and "no CUDA device" in p.stderr
+
+
+@pytest.mark.gpu
+def test_preview_sweep(tmp_path, cuda):
+    manifest = io.write_case(tmp_path / "in", *io.CASES["mixed_3tier"], sim=False)
+    assert cli("plan", "--manifest", manifest, "--out", tmp_path / "out").returncode == 0
+    doc = json.loads((tmp_path / "out" / "plan.json").read_text())
+    sweep = [dict(cost_model=dict(local_batch=b)) for b in (16, 64, 256)] + \
+            [dict(topology=dict(num_nodes=4, gpus_per_node=8))]
+    (tmp_path / "sweep.json").write_text(json.dumps(sweep))
+    p = cli("preview", "--manifest", manifest, "--plan", tmp_path / "sweep.json")
+    assert p.returncode == 0, p.stderr
+    out = json.loads(p.stdout)
+    assert len(out) == 1 + len(sweep)
+    first = out[0]["plan_3tier"]  # the manifest's own 3-tier plan
+    assert abs(first["dp_cut"] - doc["dp_cut"]) <= 1 and abs(first["flex_cut"] - doc["flex_cut"]) <= 1
+    assert [o["cost_model"]["local_batch"] for o in out[1:4]] == [16, 64, 256]
+    # larger batches make more rows worth replicating
+    assert out[1]["plan_2tier"]["dp_cut"] <= out[2]["plan_2tier"]["dp_cut"] <= out[3]["plan_2tier"]["dp_cut"]
