@@ -363,6 +363,29 @@ def run_ours(args, dist: Dist):
     loss = table.loss()
     counters = table.counters()
 
+    # ---- lookup + exchange alone (forward only) -----------
+    # the same batches, forward passes back to back (the dedup the forward
+    # prefetches for the backward is drained between passes, outside events)
+    fwd_ms = []
+    for k in range(min(args.steps, 20)):
+        b = d_rows[k % len(d_rows)] if sampler is None else None
+        if b is None:
+            occ_k = sampler.iteration(k, g * B, B, d_sampled.data_ptr(), max_occ, 0, table.stream())
+            ptr, n_occ = d_sampled.data_ptr(), occ_k
+        else:
+            ptr, n_occ = b.data_ptr(), b.numel()
+        table.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+        table.forward(ptr, n_occ, d_out.data_ptr())
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        table.synchronize()
+        fwd_ms.append(e0.elapsed_time(e1))
+    lookup_ms = dist.max(float(np.median(fwd_ms)))
+
     # ---- per-phase device times (roofline numerator) ------------------------
     table.enable_timing(True)
     prof_steps = min(args.steps, 20)
@@ -535,6 +558,19 @@ def run_ours(args, dist: Dist):
                   "frac": round(total / step_s / 1e9 / peer_peak, 4),
                   "bound_ms": round(total / (peer_peak * 1e9) * 1e3, 4)}
 
+    # lookup + exchange throughput: forward only, whole job; HBM fraction of
+    # the gather's algorithmic bytes, NVLink fraction of the forward rows
+    occ_job = dist.sum(occ_mean)
+    lookup = {"occurrences_per_s": round(occ_job / (lookup_ms / 1e3), 1),
+              "samples_per_s": round(u * B / (lookup_ms / 1e3), 1),
+              "ms_per_forward": round(lookup_ms, 4),
+              "hbm_gbs_per_gpu": round(algo["gather"] / (lookup_ms / 1e3) / 1e9, 1),
+              "hbm_frac": round(algo["gather"] / (lookup_ms / 1e3) / 1e9 / hbm_peak, 4)}
+    if u > 1:
+        fwd_rows = (off_dev["plan_global_bytes"] + off_dev["plan_intra_bytes"]) / u
+        lookup["nvlink_gbs_per_gpu"] = round(fwd_rows / (lookup_ms / 1e3) / 1e9, 1)
+        lookup["nvlink_frac"] = round(fwd_rows / (lookup_ms / 1e3) / 1e9 / 770.0, 4)
+
     cpu = None
     if dist.rank == 0 and u == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_port(batches[0], dest, plan, exp, B, D, args)
@@ -575,6 +611,7 @@ def run_ours(args, dist: Dist):
         "roofline": roofline,
         "a2a": a2a,
         "nvlink": nvlink,
+        "lookup_exchange": lookup,
         "loss_last_step": loss,
         "step_trace_ms": trace,
         **({"step_trace_ms_all_ranks": all_traces} if all_traces else {}),
