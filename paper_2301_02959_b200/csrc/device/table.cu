@@ -7,19 +7,26 @@
 //   [local_rows] fp32; remap u32[n] + placement byte u8[n] (U > 1 only — with
 //   U == 1 the local id IS the canonical index and no remap is stored).
 //
-// Forward (U == 1): one fused gather over all occurrences.
-// Forward (U > 1): bucket (DP/own -> local, RW -> owner, Flex -> node slot),
-//   stable counting pass to compact remote occurrences per destination, count
-//   all-gather + one D2H sync, NCCL all-to-allv of ids (world comm for RW,
-//   intra comm g/W for Flex), server-side gather, all-to-allv of rows back,
-//   scatter into the unpooled output.  Local occurrences are gathered
-//   directly while the exchange is in flight on the same stream order.
-// Backward: grads of remote occurrences go back to their servers (reverse
-//   all-to-allv); each server sorts (local row, source) pairs in ascending
-//   source-rank / occurrence order, segment-reduces, and applies the fused
-//   optimizer; DP rows (world) and, with N > 1, Flex rows (cross comm g%W)
-//   are reduced into dense buffers, all-reduced, then updated identically on
-//   every replica.
+// Forward (U == 1): one fused gather over all occurrences; the backward's
+//   dedup sort (it needs only the ids) starts beside it on the aux stream.
+// Forward (U > 1, one node, peer memory -- the default): bucket every
+//   occurrence (DP / own -> local, RW -> owner, Flex -> node slot), one stable
+//   counting pass compacts the remote ones per destination into request
+//   lists in HBM; one NCCL all-gather of bucket starts + output export (the
+//   step's single host sync); each server pulls its requesters' lists from
+//   their HBM and STORES the rows into their outputs over NVLink while the
+//   local rows are gathered; the dedup (entries, sort, heads) is prefetched
+//   on the aux stream.
+// Backward (peer memory): each requester stores the gradients of its remote
+//   occurrences into the servers' fixed receive buffers (then a barrier);
+//   the replicated rows' segments store their partials into the row owner's
+//   receive slots (epoch-stamped), the owner reduces them in rank order,
+//   updates and broadcasts; the rest are segment-reduced with the fused
+//   optimizer in place.
+// Staged path (no peer access, TIERSHARD_EXCHANGE=nccl): NCCL all-to-allv of
+//   ids (world comm for RW, intra comm g/W for Flex) and rows, reverse
+//   all-to-allv of gradients, dense DP (world) / Flex (cross comm g%W)
+//   all-reduce and a dense update on every replica.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
