@@ -466,7 +466,7 @@ seg_pair_kernel(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ 
     const uint32_t sb = has_b ? __ldg(starts + jb) : 0u, eb = has_b ? __ldg(starts + jb + 1) : 0u;
     const uint32_t kb = has_b ? __ldg(seg_keys + jb) : 0u;
     const bool long_a = ea - sa > short_max, long_b = has_b && eb - sb > short_max;
-    if (gl == 0) {
+    if (long_list && gl == 0) {
       if (long_a) long_list[atomicAdd(long_count, 1u)] = ja;
       if (long_b) long_list[atomicAdd(long_count, 1u)] = jb;
     }
@@ -529,8 +529,8 @@ seg_short_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__
   const uint64_t col = static_cast<uint64_t>(gl) * PER;
   for (uint32_t j = seg_lo + gid; j < seg_hi; j += ngroups) {
     const uint32_t s = __ldg(starts + j), e = __ldg(starts + j + 1);
-    if (e - s > short_max) {
-      if (gl == 0) long_list[atomicAdd(long_count, 1u)] = j;
+    if (e - s > short_max) {  // listed here, or beforehand (long_list == nullptr)
+      if (long_list && gl == 0) long_list[atomicAdd(long_count, 1u)] = j;
       continue;
     }
     const uint32_t row = __ldg(keys + s);
@@ -556,6 +556,28 @@ seg_short_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__
     group_finish_row<DIM>(row, acc, gl, gmask, weights, state, opt, d0, d1);
   }
   if (d0.push_n | d1.push_n) __threadfence_system();  // partials stored to peers
+}
+
+// Segments [*d_lo, *d_hi) longer than short_max entries -> long_list (warp
+// ballot + one atomic per warp), so the piece path can start without waiting
+// for the short kernel to discover them.
+__global__ void __launch_bounds__(kThreads)
+long_segments_kernel(const uint32_t* __restrict__ starts, const uint32_t* __restrict__ d_lo,
+                     const uint32_t* __restrict__ d_hi, uint32_t short_max,
+                     uint32_t* __restrict__ long_list, uint32_t* __restrict__ long_count) {
+  const uint32_t lo = *d_lo, hi = *d_hi;
+  const unsigned lane = threadIdx.x & 31u;
+  const uint32_t stride = gridDim.x * kThreads;
+  for (uint32_t base = lo + (blockIdx.x * kThreads + threadIdx.x - lane); base < hi; base += stride) {
+    const uint32_t j = base + lane;
+    const bool is_long = j < hi && __ldg(starts + j + 1) - __ldg(starts + j) > short_max;
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, is_long);
+    if (!b) continue;
+    uint32_t pos = 0;
+    if (lane == 0) pos = atomicAdd(long_count, static_cast<uint32_t>(__popc(b)));
+    pos = __shfl_sync(0xFFFFFFFFu, pos, 0);
+    if (is_long) long_list[pos + __popc(b & ((1u << lane) - 1u))] = j;
+  }
 }
 
 // piece_off[i] = exclusive prefix of pieces over the long list.
@@ -890,7 +912,7 @@ void launch_segment_update(const uint32_t* keys, const uint32_t* vals, const uin
                            const DenseRange& dense1, const SegmentScratch& sc,
                            cudaStream_t stream) {
   if (n_entries == 0) return;
-  TSD_CUDA(cudaMemsetAsync(sc.long_count, 0, sizeof(uint32_t), stream));
+  if (sc.long_list) TSD_CUDA(cudaMemsetAsync(sc.long_count, 0, sizeof(uint32_t), stream));
   const unsigned grid = persistent_grid(g_compute_blocks_per_sm);
   dispatch_dim(dim, [&](auto D) {
     constexpr int DIM = decltype(D)::value;
@@ -922,8 +944,10 @@ void launch_segment_long(const uint32_t* keys, const uint32_t* vals, const uint3
   const unsigned grid = persistent_grid(g_compute_blocks_per_sm);
   dispatch_dim(dim, [&](auto D) {
     constexpr int DIM = decltype(D)::value;
-    long_prefix_kernel<<<1, 1024, 0, stream>>>(sc.long_list, sc.long_count, starts, sc.piece_off);
-    TSD_LAUNCH_CHECK();
+    if (!sc.prefixed) {
+      long_prefix_kernel<<<1, 1024, 0, stream>>>(sc.long_list, sc.long_count, starts, sc.piece_off);
+      TSD_LAUNCH_CHECK();
+    }
     piece_kernel<DIM><<<grid, kThreads, 0, stream>>>(keys, vals, starts, sc.long_list, sc.long_count,
                                                      sc.piece_off, grads, sc.partials, weights, state, opt,
                                                      dense0, dense1);
@@ -934,6 +958,18 @@ void launch_segment_long(const uint32_t* keys, const uint32_t* vals, const uint3
                                                             dense0, dense1);
     TSD_LAUNCH_CHECK();
   });
+}
+
+void launch_long_segments(const uint32_t* starts, const uint32_t* d_lo, const uint32_t* d_hi,
+                          uint64_t n_entries, const SegmentScratch& sc, cudaStream_t stream) {
+  TSD_CUDA(cudaMemsetAsync(sc.long_count, 0, sizeof(uint32_t), stream));
+  const unsigned grid = std::max<unsigned>(
+      1, std::min<unsigned>(persistent_grid(4), static_cast<unsigned>(ceil_div(n_entries, kThreads))));
+  long_segments_kernel<<<grid, kThreads, 0, stream>>>(starts, d_lo, d_hi, sc.short_max, sc.long_list,
+                                                      sc.long_count);
+  TSD_LAUNCH_CHECK();
+  long_prefix_kernel<<<1, 1024, 0, stream>>>(sc.long_list, sc.long_count, starts, sc.piece_off);
+  TSD_LAUNCH_CHECK();
 }
 
 void launch_dense_update(const float* grad, uint32_t rows, uint32_t row_lo, uint32_t dim,

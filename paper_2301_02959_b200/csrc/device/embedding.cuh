@@ -91,6 +91,7 @@ struct SegmentScratch {
   uint32_t max_long = 0;
   uint32_t max_pieces = 0;
   uint32_t short_max = kPiece;     // longer segments take the piece path
+  bool prefixed = false;           // piece_off already built (launch_long_segments)
 };
 
 // Segments [*d_lo, *d_hi) (device scalars, so ranges can be chosen on the
@@ -108,6 +109,13 @@ void launch_segment_long(const uint32_t* keys, const uint32_t* vals, const uint3
                          float* state, const OptParams& opt, const DenseRange& dense0,
                          const DenseRange& dense1, const SegmentScratch& scratch,
                          cudaStream_t stream);
+
+// Lists the segments of [*d_lo, *d_hi) longer than scratch.short_max and
+// builds piece_off, ahead of the segment update: then launch_segment_update
+// runs with scratch.long_list == nullptr (skip long segments, list nothing)
+// and launch_segment_long with scratch.prefixed, on another stream.
+void launch_long_segments(const uint32_t* starts, const uint32_t* d_lo, const uint32_t* d_hi,
+                          uint64_t n_entries, const SegmentScratch& scratch, cudaStream_t stream);
 
 // out[0] = 0, out[1] = number of segments whose key < split_key.
 void launch_segment_split(const uint32_t* keys, const uint32_t* starts, const uint32_t* d_nseg,

@@ -122,6 +122,20 @@ struct ts_table {
   bool dedup_in_forward = true;
   uint32_t seg_short_max = tsd::kPiece;  // tsd::short_max(U), set at creation
   bool dedup_ready = false;
+  // U = 1: segments longer than seg_short_max are listed with the dedup, and
+  // their piece path runs on `aux` beside the short-segment kernel
+  // (TIERSHARD_LONG_CONCURRENT=0 keeps both on the compute stream).
+  bool long_concurrent = true;
+  cudaEvent_t ev_seg0 = nullptr, ev_long = nullptr;
+  tsd::SegmentScratch seg_scratch_view() const {
+    tsd::SegmentScratch sc;
+    sc.long_list = long_list.ptr;
+    sc.long_count = long_count.ptr;
+    sc.piece_off = piece_off.ptr;
+    sc.partials = partials.ptr;
+    sc.short_max = seg_short_max;
+    return sc;
+  }
   uint32_t* dd_keys = nullptr;
   uint32_t* dd_vals = nullptr;
   unsigned fwd_gather_grid = 0;
@@ -345,9 +359,23 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
   {
     if (const char* e = std::getenv("TIERSHARD_DEDUP_IN_FORWARD")) dedup_in_forward = std::string(e) != "0";
     if (dedup_in_forward) {
-      TSD_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+      // aux priority (TIERSHARD_AUX_PRIORITY=high|low): at U = 1 the dedup
+      // sort's blocks are dispatched ahead of the gather's (measured at C2
+      // with 6 gather blocks per SM: 1.328 -> 1.307 ms/step); at U > 1 the
+      // comm stream holds the high priority
+      const char* pe = std::getenv("TIERSHARD_AUX_PRIORITY");
+      const bool aux_high = pe ? std::string(pe) == "high" : U == 1;
+      int lo_pri = 0, hi_pri = 0;
+      TSD_CUDA(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+      TSD_CUDA(cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, aux_high ? hi_pri : lo_pri));
       TSD_CUDA(cudaEventCreateWithFlags(&ev_fwd0, cudaEventDisableTiming));
       TSD_CUDA(cudaEventCreateWithFlags(&ev_dedup, cudaEventDisableTiming));
+    }
+    if (const char* e = std::getenv("TIERSHARD_LONG_CONCURRENT")) long_concurrent = std::string(e) != "0";
+    long_concurrent = long_concurrent && aux && U == 1;
+    if (long_concurrent) {
+      TSD_CUDA(cudaEventCreateWithFlags(&ev_seg0, cudaEventDisableTiming));
+      TSD_CUDA(cudaEventCreateWithFlags(&ev_long, cudaEventDisableTiming));
     }
   }
 
@@ -410,7 +438,9 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
   fwd_gather_grid = gather_grid;
   if (aux) {
     const char* e = std::getenv("TIERSHARD_GATHER_BLOCKS");
-    const unsigned per_sm = e ? static_cast<unsigned>(std::max(1, std::atoi(e))) : 8u;
+    // 6 blocks per SM leave the dedup sort room beside the gather (C2, N=1:
+    // 8 -> 1.318 ms/step, 6 -> 1.307, 4 -> 1.328; aux at high priority)
+    const unsigned per_sm = e ? static_cast<unsigned>(std::max(1, std::atoi(e))) : 6u;
     fwd_gather_grid = std::min(gather_grid, static_cast<unsigned>(tsd::sm_count()) * per_sm);
   }
   // [local gather partials | remote partials: staged scatter (gather_grid) or
@@ -615,6 +645,7 @@ void ts_table::dedup_local(cudaStream_t on) {
   t = phase_begin(kPhaseSegments, on);
   segment_starts(dd_keys, last_occ, starts.ptr, seg_keys.ptr, nseg.ptr, seg_scratch.ptr, on);
   TSD_CUDA(cudaMemsetAsync(seg_split.ptr, 0, sizeof(uint32_t), on));  // range [0, nseg)
+  if (long_concurrent) launch_long_segments(starts.ptr, seg_split.ptr, nseg.ptr, last_occ, seg_scratch_view(), on);
   phase_end(t);
 }
 
@@ -797,6 +828,26 @@ void ts_table::backward(const float* d_grad) {
     }
     sk = dd_keys;
     sv = dd_vals;
+    if (long_concurrent) {
+      // long segments (listed with the dedup) on aux, short ones here: they
+      // update disjoint rows, and each kernel's tail fills the other's
+      TSD_CUDA(cudaEventRecord(ev_seg0, stream));  // gradients + dedup ready
+      TSD_CUDA(cudaStreamWaitEvent(aux, ev_seg0, 0));
+      SegmentScratch lsc = sc;
+      lsc.prefixed = true;
+      int t = phase_begin(kPhaseSegmentLong, aux);
+      launch_segment_long(sk, sv, starts.ptr, occ, cfg.dim, gs, d_w, d_state, opt, d0, d1, lsc, aux);
+      phase_end(t);
+      TSD_CUDA(cudaEventRecord(ev_long, aux));
+      SegmentScratch ssc = sc;
+      ssc.long_list = nullptr;  // listed already: skip, list nothing
+      t = phase_begin(kPhaseSegmentUpdate);
+      launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr, nseg.ptr, occ, cfg.dim, gs, d_w,
+                            d_state, opt, d0, d1, ssc, stream);
+      phase_end(t);
+      TSD_CUDA(cudaStreamWaitEvent(stream, ev_long, 0));
+      return;
+    }
     int t = phase_begin(kPhaseSegmentUpdate);
     launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr, nseg.ptr, occ, cfg.dim, gs, d_w, d_state,
                           opt, d0, d1, sc, stream);
@@ -1248,7 +1299,7 @@ void ts_table::destroy() {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
   }
-  for (cudaEvent_t e : {ev_ids, ev_fwd, ev_bwd0, ev_grads, ev_dense, ev_ar, ev_fwd0, ev_dedup}) {
+  for (cudaEvent_t e : {ev_ids, ev_fwd, ev_bwd0, ev_grads, ev_dense, ev_ar, ev_fwd0, ev_dedup, ev_seg0, ev_long}) {
     if (e) cudaEventDestroy(e);
   }
   if (aux) {
