@@ -122,9 +122,10 @@ struct ts_table {
   bool dedup_in_forward = true;
   uint32_t seg_short_max = tsd::kPiece;  // tsd::short_max(U), set at creation
   bool dedup_ready = false;
-  // U = 1: segments longer than seg_short_max are listed with the dedup, and
-  // their piece path runs on `aux` beside the short-segment kernel
-  // (TIERSHARD_LONG_CONCURRENT=0 keeps both on the compute stream).
+  // Segments longer than seg_short_max are listed ahead of the segment
+  // update (U = 1: with the dedup in the forward; U > 1: per segment range,
+  // on aux) and their piece path runs on `aux` beside the short-segment
+  // kernel (TIERSHARD_LONG_CONCURRENT=0 keeps both on the compute stream).
   bool long_concurrent = true;
   cudaEvent_t ev_seg0 = nullptr, ev_long = nullptr;
   tsd::SegmentScratch seg_scratch_view() const {
@@ -313,6 +314,10 @@ struct ts_table {
   void create(const ts_table_config& c, const uint8_t* tier_dest);
   void dedup_local(cudaStream_t on);
   void dedup_p2p(cudaStream_t on);
+  void segment_range_concurrent(const uint32_t* sk, const uint32_t* sv, const uint32_t* d_lo,
+                                const uint32_t* d_hi, uint64_t m, const tsd::GradSource& gs,
+                                const tsd::OptParams& opt, const tsd::DenseRange& d0,
+                                const tsd::DenseRange& d1);
   void forward(const uint32_t* d_rows, uint64_t occ, float* d_out);
   void backward(const float* d_grad);
   void exchange(const void* send, const std::vector<uint64_t>& s_off,
@@ -372,7 +377,7 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
       TSD_CUDA(cudaEventCreateWithFlags(&ev_dedup, cudaEventDisableTiming));
     }
     if (const char* e = std::getenv("TIERSHARD_LONG_CONCURRENT")) long_concurrent = std::string(e) != "0";
-    long_concurrent = long_concurrent && aux && U == 1;
+    long_concurrent = long_concurrent && aux;
     if (long_concurrent) {
       TSD_CUDA(cudaEventCreateWithFlags(&ev_seg0, cudaEventDisableTiming));
       TSD_CUDA(cudaEventCreateWithFlags(&ev_long, cudaEventDisableTiming));
@@ -645,7 +650,9 @@ void ts_table::dedup_local(cudaStream_t on) {
   t = phase_begin(kPhaseSegments, on);
   segment_starts(dd_keys, last_occ, starts.ptr, seg_keys.ptr, nseg.ptr, seg_scratch.ptr, on);
   TSD_CUDA(cudaMemsetAsync(seg_split.ptr, 0, sizeof(uint32_t), on));  // range [0, nseg)
-  if (long_concurrent) launch_long_segments(starts.ptr, seg_split.ptr, nseg.ptr, last_occ, seg_scratch_view(), on);
+  if (long_concurrent && U == 1) {
+    launch_long_segments(starts.ptr, seg_split.ptr, nseg.ptr, last_occ, seg_scratch_view(), on);
+  }
   phase_end(t);
 }
 
@@ -1066,6 +1073,32 @@ void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
                        stream);
 }
 
+// Segments [*d_lo, *d_hi): short ones on the compute stream, long ones listed
+// and reduced on aux beside them (disjoint rows); the compute stream joins.
+void ts_table::segment_range_concurrent(const uint32_t* sk, const uint32_t* sv, const uint32_t* d_lo,
+                                        const uint32_t* d_hi, uint64_t m, const tsd::GradSource& gs,
+                                        const tsd::OptParams& opt, const tsd::DenseRange& d0,
+                                        const tsd::DenseRange& d1) {
+  using namespace tsd;
+  const SegmentScratch sc = seg_scratch_view();
+  TSD_CUDA(cudaEventRecord(ev_seg0, stream));  // gradients + segments ready
+  TSD_CUDA(cudaStreamWaitEvent(aux, ev_seg0, 0));
+  int t = phase_begin(kPhaseSegmentLong, aux);
+  launch_long_segments(starts.ptr, d_lo, d_hi, m, sc, aux);
+  SegmentScratch lsc = sc;
+  lsc.prefixed = true;
+  launch_segment_long(sk, sv, starts.ptr, m, cfg.dim, gs, d_w, d_state, opt, d0, d1, lsc, aux);
+  phase_end(t);
+  TSD_CUDA(cudaEventRecord(ev_long, aux));
+  SegmentScratch ssc = sc;
+  ssc.long_list = nullptr;
+  t = phase_begin(kPhaseSegmentUpdate);
+  launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, d_lo, d_hi, m, cfg.dim, gs, d_w, d_state, opt, d0, d1,
+                        ssc, stream);
+  phase_end(t);
+  TSD_CUDA(cudaStreamWaitEvent(stream, ev_long, 0));
+}
+
 void ts_table::backward_p2p(const float* d_grad) {
   using namespace tsd;
   const uint64_t occ = last_occ;
@@ -1196,13 +1229,17 @@ void ts_table::backward_p2p(const float* d_grad) {
   // without the remote rows; Flex rows replicated across nodes need them.
   const bool dense_needs_remote = N > 1 && flex_rows;
   if (dense_needs_remote) TSD_CUDA(cudaStreamWaitEvent(stream, ev_grads, 0));
-  t = phase_begin(kPhaseSegmentUpdate);
-  launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr, seg_split.ptr + 1, m, cfg.dim, gs, d_w, d_state,
-                        opt, d0, d1, sc, stream);
-  phase_end(t);
-  t = phase_begin(kPhaseSegmentLong);
-  launch_segment_long(sk, sv, starts.ptr, m, cfg.dim, gs, d_w, d_state, opt, d0, d1, sc, stream);
-  phase_end(t);
+  if (long_concurrent) {
+    segment_range_concurrent(sk, sv, seg_split.ptr, seg_split.ptr + 1, m, gs, opt, d0, d1);
+  } else {
+    t = phase_begin(kPhaseSegmentUpdate);
+    launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr, seg_split.ptr + 1, m, cfg.dim, gs, d_w,
+                          d_state, opt, d0, d1, sc, stream);
+    phase_end(t);
+    t = phase_begin(kPhaseSegmentLong);
+    launch_segment_long(sk, sv, starts.ptr, m, cfg.dim, gs, d_w, d_state, opt, d0, d1, sc, stream);
+    phase_end(t);
+  }
   if (!dense_needs_remote) TSD_CUDA(cudaStreamWaitEvent(stream, ev_grads, 0));
   // ---- replicated tiers over peer memory: after a rendezvous (all ranks'
   // partials written), each rank reduces its slice of the replicated rows in
@@ -1253,13 +1290,17 @@ void ts_table::backward_p2p(const float* d_grad) {
   }
   phase_end(t);
   if (replica_concurrent) TSD_CUDA(cudaEventRecord(ev_ar, comm));
-  t = phase_begin(kPhaseSegmentUpdate);
-  launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr + 1, nseg.ptr, m, cfg.dim, gs, d_w, d_state, opt,
-                        d0, d1, sc, stream);
-  phase_end(t);
-  t = phase_begin(kPhaseSegmentLong);
-  launch_segment_long(sk, sv, starts.ptr, m, cfg.dim, gs, d_w, d_state, opt, d0, d1, sc, stream);
-  phase_end(t);
+  if (long_concurrent) {
+    segment_range_concurrent(sk, sv, seg_split.ptr + 1, nseg.ptr, m, gs, opt, d0, d1);
+  } else {
+    t = phase_begin(kPhaseSegmentUpdate);
+    launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr + 1, nseg.ptr, m, cfg.dim, gs, d_w,
+                          d_state, opt, d0, d1, sc, stream);
+    phase_end(t);
+    t = phase_begin(kPhaseSegmentLong);
+    launch_segment_long(sk, sv, starts.ptr, m, cfg.dim, gs, d_w, d_state, opt, d0, d1, sc, stream);
+    phase_end(t);
+  }
   if (replica_concurrent) TSD_CUDA(cudaStreamWaitEvent(stream, ev_ar, 0));
   // peers store into our replicated rows: the next step's rendezvous (its
   // all-gather on the comm stream, after this stream's work) orders those
