@@ -61,7 +61,8 @@ def run_ranks(u, worker_args, env=None):
 
 CASES = [(1, 2, 1, "p2p"), (2, 1, 1, "p2p"), (2, 1, 0, "p2p"), (2, 2, 1, "p2p"), (1, 4, 1, "p2p"),
          (1, 2, 1, "p2p_pull"), (2, 2, 1, "p2p_pull"), (1, 4, 0, "p2p_pull"),
-         (1, 2, 1, "nccl"), (2, 2, 1, "nccl"), (2, 1, 0, "nccl")]
+         (1, 2, 1, "nccl"), (2, 2, 1, "nccl"), (2, 1, 0, "nccl"),
+         (1, 2, 1, "p2p_short8"), (2, 2, 1, "p2p_short8"), (1, 2, 1, "p2p_serial")]
 
 
 @pytest.mark.parametrize("n_nodes,w,opt,exchange", CASES)
@@ -69,12 +70,17 @@ def test_multi_gpu_matches_oracle(cuda, tmp_path, n_nodes, w, opt, exchange):
     """exchange: "p2p" = peer-memory serve + gradient push (default on one
     node), "p2p_pull" = servers gather remote gradients with peer loads
     (TIERSHARD_GRADS=pull), "nccl" = staged NCCL all-to-allv
-    (TIERSHARD_EXCHANGE=nccl)."""
+    (TIERSHARD_EXCHANGE=nccl), "p2p_short8" = segments over 8 entries take
+    the piece path on the aux stream (TIERSHARD_SHORT_MAX=8), "p2p_serial" =
+    long segments after the short kernel (TIERSHARD_LONG_CONCURRENT=0)."""
     u = n_nodes * w
     if n_devices() < u:
         pytest.skip(f"needs {u} GPUs")
     env = dict(os.environ, TIERSHARD_EXCHANGE="nccl" if exchange == "nccl" else "p2p",
-               TIERSHARD_GRADS="pull" if exchange == "p2p_pull" else "push")
+               TIERSHARD_GRADS="pull" if exchange == "p2p_pull" else "push",
+               TIERSHARD_LONG_CONCURRENT="0" if exchange == "p2p_serial" else "1")
+    if exchange == "p2p_short8":
+        env["TIERSHARD_SHORT_MAX"] = "8"
     proc = run_ranks(u, ["--nodes", str(n_nodes), "--gpus-per-node", str(w), "--optimizer", str(opt),
                          "--lr", str(LR), "--out", str(tmp_path)], env)
     assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]

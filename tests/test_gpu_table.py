@@ -159,3 +159,36 @@ def test_bad_config_rejected(cuda):
     with pytest.raises(ts.TSError) as e:
         ts.Table(n_rows=100, dim=64, dp_cut=50, flex_cut=10)
     assert e.value.kind == "ValidationError"
+
+
+@pytest.mark.parametrize("schedule", [
+    {"TIERSHARD_LONG_CONCURRENT": "1"},
+    {"TIERSHARD_LONG_CONCURRENT": "0"},
+    {"TIERSHARD_LONG_CONCURRENT": "1", "TIERSHARD_SHORT_MAX": "8"},
+    {"TIERSHARD_LONG_CONCURRENT": "1", "TIERSHARD_SHORT_MAX": "256"},
+    {"TIERSHARD_DEDUP_IN_FORWARD": "0"},  # no aux stream: everything serial
+])
+def test_segment_schedules_bit_exact(cuda, monkeypatch, schedule):
+    """Every segment schedule (long segments beside the short kernel on the aux
+    stream or after it, the short/long threshold, dedup in the forward or the
+    backward) gives the oracle's weights bit for bit over three steps."""
+    import paper_2301_02959_b200 as ts
+    for k, v in schedule.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(21)
+    n, dim, occ = 5000, 128, 20000
+    lr = 0.05
+    table = ts.Table(n_rows=n, dim=dim, dp_cut=0, flex_cut=0, weight_seed=SEED,
+                     optimizer=orc.OPT_ROWWISE_ADAGRAD, lr=lr, max_occurrences=occ)
+    w = orc.init_table(SEED, n, dim)
+    state = np.zeros(n, np.float32)
+    for step in range(3):
+        rows = zipf_rows(rng, n, occ, hot=[(1, 3000), (9, 600), (2500, 40)])
+        loss = table.train_step_host(rows)
+        expect = orc.gather(w, rows)
+        assert loss == pytest.approx(orc.half_sq_sum(expect), rel=1e-6)
+        orc.backward_update(w, state, rows, expect, orc.OPT_ROWWISE_ADAGRAD, lr, 1e-8)
+    got, got_state = table.read_rows(np.arange(n, dtype=np.uint32), with_state=True)
+    assert np.array_equal(got.view(np.uint32), w.view(np.uint32))
+    assert np.array_equal(got_state.view(np.uint32), state.view(np.uint32))
+    table.close()
