@@ -444,8 +444,10 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
   if (aux) {
     const char* e = std::getenv("TIERSHARD_GATHER_BLOCKS");
     // 6 blocks per SM leave the dedup sort room beside the gather (C2, N=1:
-    // 8 -> 1.318 ms/step, 6 -> 1.307, 4 -> 1.328; aux at high priority)
-    const unsigned per_sm = e ? static_cast<unsigned>(std::max(1, std::atoi(e))) : 6u;
+    // 8 -> 1.318 ms/step, 6 -> 1.307, 4 -> 1.328; aux at high priority).  At
+    // U > 1 8 stays best (N=2: 2.33 ms against 2.35-2.36 with 6; a high-
+    // priority aux there costs 0.1 ms: the sort then delays serve and push)
+    const unsigned per_sm = e ? static_cast<unsigned>(std::max(1, std::atoi(e))) : (U == 1 ? 6u : 8u);
     fwd_gather_grid = std::min(gather_grid, static_cast<unsigned>(tsd::sm_count()) * per_sm);
   }
   // [local gather partials | remote partials: staged scatter (gather_grid) or
@@ -1066,7 +1068,7 @@ void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   TSD_CUDA(cudaEventRecord(ev_fwd, comm));
 
   t = phase_begin(kPhaseGather);
-  launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, gather_grid, stream);
+  launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, fwd_gather_grid, stream);
   phase_end(t);
   TSD_CUDA(cudaStreamWaitEvent(stream, ev_fwd, 0));
   launch_loss_finalize(loss_partials.ptr, static_cast<unsigned>(gather_grid + remote_loss_slots), d_loss.ptr,
