@@ -652,9 +652,6 @@ void ts_table::dedup_local(cudaStream_t on) {
   t = phase_begin(kPhaseSegments, on);
   segment_starts(dd_keys, last_occ, starts.ptr, seg_keys.ptr, nseg.ptr, seg_scratch.ptr, on);
   TSD_CUDA(cudaMemsetAsync(seg_split.ptr, 0, sizeof(uint32_t), on));  // range [0, nseg)
-  if (long_concurrent && U == 1) {
-    launch_long_segments(starts.ptr, seg_split.ptr, nseg.ptr, last_occ, seg_scratch_view(), on);
-  }
   phase_end(t);
 }
 
@@ -708,6 +705,9 @@ void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
       TSD_CUDA(cudaStreamWaitEvent(aux, ev_fwd0, 0));
       dedup_local(aux);
       TSD_CUDA(cudaEventRecord(ev_dedup, aux));
+      // the long-segment list is needed only by the backward's aux work: it
+      // stays off the chain the short-segment kernel waits for
+      if (long_concurrent) launch_long_segments(starts.ptr, seg_split.ptr, nseg.ptr, occ, seg_scratch_view(), aux);
       dedup_ready = true;
     }
     return;
@@ -834,6 +834,7 @@ void ts_table::backward(const float* d_grad) {
       dedup_ready = false;
     } else {
       dedup_local(stream);
+      if (long_concurrent) launch_long_segments(starts.ptr, seg_split.ptr, nseg.ptr, occ, seg_scratch_view(), stream);
     }
     sk = dd_keys;
     sv = dd_vals;
