@@ -913,7 +913,17 @@ void launch_segment_update(const uint32_t* keys, const uint32_t* vals, const uin
                            cudaStream_t stream) {
   if (n_entries == 0) return;
   if (sc.long_list) TSD_CUDA(cudaMemsetAsync(sc.long_count, 0, sizeof(uint32_t), stream));
-  const unsigned grid = persistent_grid(g_compute_blocks_per_sm);
+  // with the long path concurrent (long_list == nullptr) the short kernel's
+  // grid can leave SM slots to it: TIERSHARD_SHORT_BLOCKS blocks per SM.
+  // Measured at C2, N=1 (4 resident at 64 registers): 8 -> 1.308 ms/step
+  // (the piece kernel starts once first-wave blocks retire), 4 -> 1.322 (it
+  // starts only at the end), 3 -> 1.305 (both run side by side and end
+  // together), 2 -> 1.399.  Default: the compute grid (8 per SM).
+  static const unsigned short_blocks = [] {
+    const char* e = std::getenv("TIERSHARD_SHORT_BLOCKS");
+    return e ? static_cast<unsigned>(std::max(1, std::atoi(e))) : 0u;
+  }();
+  const unsigned grid = persistent_grid(!sc.long_list && short_blocks ? short_blocks : g_compute_blocks_per_sm);
   dispatch_dim(dim, [&](auto D) {
     constexpr int DIM = decltype(D)::value;
     if (seg_variant() == 0 || DIM > 128) {
