@@ -1,0 +1,9 @@
+#!/bin/bash
+# N=1 A/B of the U=1 grids: gather blocks per SM (beside the sort) and short-kernel blocks per SM.
+for v in "TIERSHARD_GATHER_BLOCKS=6" "TIERSHARD_GATHER_BLOCKS=5" "TIERSHARD_GATHER_BLOCKS=7" \
+         "TIERSHARD_GATHER_BLOCKS=6 TIERSHARD_SHORT_BLOCKS=3" "TIERSHARD_GATHER_BLOCKS=5 TIERSHARD_SHORT_BLOCKS=3" \
+         "TIERSHARD_GATHER_BLOCKS=6" "TIERSHARD_GATHER_BLOCKS=6 TIERSHARD_SHORT_BLOCKS=3"; do
+  env $v timeout 600 python bench.py --steps 50 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/ab.json 2>/dev/null
+  python -c "
+import json;d=json.loads(open('gpurun_out/ab.json').read().splitlines()[-1]);print('$v', d['value'], d['ms_per_step'], d['step_ms_min_median_max_rank0'], d['roofline']['all_phases_ms_per_step'])"
+done
