@@ -248,7 +248,7 @@ PHASE_KERNELS = {
 def ncu_traffic(phase, u):
     """DRAM bytes (read + write) per launch of the phase's kernels, from the
     committed ncu --set full capture summarised in profiles/ncu_traffic.json
-    (tools_traffic.py).  None when that capture does not cover the phase."""
+    (tools/traffic.py).  None when that capture does not cover the phase."""
     try:
         doc = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
     except Exception:

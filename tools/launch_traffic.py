@@ -3,7 +3,7 @@
 per kernel launches, average time, share of GPU time, DRAM bytes per launch
 and DRAM GB/s (cold-cache, serialised launches: shares, not absolutes).
 
-    python tools_launch_traffic.py launches.csv [OUT.txt]
+    python tools/launch_traffic.py launches.csv [OUT.txt]
 """
 import collections
 import csv

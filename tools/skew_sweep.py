@@ -7,7 +7,7 @@ D = 128, L = 128 per table, batch 4096 per GPU).  Host only: the planner and
 placement are the product's (bit-exact with the reference); traffic is
 counted per occurrence by bin/ts_driver's export.
 
-    python tools_skew_sweep.py OUT.json [--rows N]
+    python tools/skew_sweep.py OUT.json [--rows N]
 """
 import argparse
 import json
@@ -15,7 +15,7 @@ import subprocess
 import tempfile
 from pathlib import Path
 
-ROOT = Path(__file__).resolve().parent
+ROOT = Path(__file__).resolve().parent.parent
 DRIVER = ROOT / "paper_2301_02959_b200" / "bin" / "ts_driver"
 HOMO = dict(a2a_global_gibs=1, a2a_intra_gibs=1, ar_global_gibs=1, ar_cross_gibs=1)
 PAPER_BW = dict(a2a_global_gibs=23, a2a_intra_gibs=95, ar_global_gibs=73, ar_cross_gibs=15)

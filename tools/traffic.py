@@ -2,7 +2,7 @@
 (read + write) per launch of every kernel, summed per bench phase (one step's
 launches of that phase).  bench.py reports it as roofline.traffic.
 
-    python tools_traffic.py OUT.json source-label REPORT.ncu-rep [...]
+    python tools/traffic.py OUT.json source-label REPORT.ncu-rep [...]
 """
 import collections
 import csv
