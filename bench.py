@@ -42,7 +42,7 @@ HOMO = dict(a2a_global_gibs=1, a2a_intra_gibs=1, ar_global_gibs=1, ar_cross_gibs
 PAPER_BW = dict(a2a_global_gibs=23, a2a_intra_gibs=95, ar_global_gibs=73, ar_cross_gibs=15)
 
 
-def parse_args():
+def parse_args(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=50)
@@ -60,12 +60,13 @@ def parse_args():
     p.add_argument("--virtual-nodes", action="store_true", help="2 x N/2 virtual nodes, paper bw, 3-tier")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-routing", action="store_true", help="skip the logical-U=8 routing record (N=1)")
     p.add_argument("--sampler", choices=("host", "gpu"), default="host",
                    help="host: the reference Workload's batches (bit-exact), materialized once and "
                         "cycled; gpu: each step's batch drawn on the GPU inside the timed region "
                         "(ts_sampler, same law, for C4/C5-scale throughput runs)")
     p.add_argument("--cache", default="/tmp/tiershard_bench")
-    return p.parse_args()
+    return p.parse_args(argv)
 
 
 # --------------------------------------------------------------------------
@@ -144,13 +145,31 @@ def workload_spec(args, n_gpus):
                 export_alias=args.sampler == "gpu")
 
 
-def prepare(args, dist: Dist, n_gpus):
+def job_config(args, u, w, goal, dp_cut, flex_cut):
+    """The workload identity both arms print (identical dicts => the driver's
+    same_config).  Arm-specific run details go under "run"."""
+    c2 = (args.tables, args.rows, args.seq_len, args.dim, args.batch) == (8, 10_000_000, 128, 128, 4096)
+    return {
+        "workload": f"{'C2' if c2 else 'custom'}: {args.tables} tables x {args.rows} rows x D={args.dim} fp32, "
+                    f"seq len {args.seq_len}/table, batch {args.batch}/GPU, Zipf {args.exponent}",
+        "topology": f"{u // w} x {w}" + (" virtual nodes, paper bw" if args.virtual_nodes and u // w > 1
+                                         else " homogeneous"),
+        "plan": goal, "dp_cut": dp_cut, "flex_cut": flex_cut,
+        "global_batch": u * args.batch, "seq_len": args.seq_len * args.tables,
+        "parallelism": f"row-sharded over {u} GPU(s): DP/Flex/RW tiers",
+        "optimizer": args.optimizer,
+        "l2": "GPU arm: 256 MiB written between timed steps (outside the events); tables 41 GB >> L2",
+    }
+
+
+def prepare(args, dist, n_gpus):
     from paper_2301_02959_b200 import DRIVER_PATH
     spec = workload_spec(args, n_gpus)
     key = hashlib.sha1(json.dumps(spec, sort_keys=True).encode()).hexdigest()[:16]
     out_dir = Path(args.cache) / key
     meta_path = out_dir / "meta.json"
-    if dist.rank == 0 and not meta_path.exists():
+    rank0 = dist is None or dist.rank == 0
+    if rank0 and not meta_path.exists():
         out_dir.mkdir(parents=True, exist_ok=True)
         spec_run = dict(spec, export_dir=str(out_dir))
         (out_dir / "spec.json").write_text(json.dumps(spec_run))
@@ -162,7 +181,8 @@ def prepare(args, dist: Dist, n_gpus):
             raise RuntimeError(doc)
         doc["prep_wall_s"] = time.time() - t0
         meta_path.write_text(json.dumps(doc))
-    dist.barrier()
+    if dist is not None:
+        dist.barrier()
     doc = json.loads(meta_path.read_text())
     return spec, out_dir, doc
 
@@ -266,6 +286,77 @@ def measured_peaks():
         return {}
 
 
+def measure_p2p_ceiling(u):
+    """tools/p2p_bw --json on the job's GPUs (every GPU storing 512 B rows
+    into random slots of every peer at once): the NVLink ceiling for the
+    exchange kernels' access pattern, measured on this box in this run."""
+    tool = ROOT / "tools" / "p2p_bw"
+    if not tool.exists():
+        return None
+    try:
+        out = subprocess.run([str(tool), str(u), "--json"], capture_output=True, text=True, timeout=300)
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001 - reported, the fallback peak is labelled
+        return {"error": repr(e)}
+
+
+def nvlink_peak(ceiling):
+    if ceiling and ceiling.get("gather_store_gbs"):
+        return float(ceiling["gather_store_gbs"]), ("tools/p2p_bw gather_store (all-to-all 512 B row stores, "
+                                                     "every GPU at once), measured in this run")
+    return 770.0, "fallback: B200_PROFILING.md peer copy per direction (p2p_bw unavailable)"
+
+
+def run_routing(args, dist):
+    """The reference's routing loop (simulator.cpp:223-257) on the GPU for a
+    whole LOGICAL iteration of the C2 job at U = 8 -- 1 x 8 (2-tier) and
+    2 x 4 virtual nodes (3-tier) -- device-resident: ts_router_iteration_device,
+    event-timed.  Bytes model: 4 B index + 1 B placement byte per occurrence
+    (the bitmap clears, U x n bits, are timed separately)."""
+    import torch
+    import paper_2301_02959_b200 as ts
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    res = {}
+    for label, vn in (("1x8", False), ("2x4", True)):
+        a = argparse.Namespace(**vars(args))
+        a.iterations, a.sampler, a.virtual_nodes = 1, "host", vn
+        _, ddir, doc = prepare(a, None, 8)
+        exp, plan = doc["export"], doc["plan"]
+        u, w, B = exp["num_gpus"], exp["gpus_per_node"], exp["local_batch"]
+        dest = np.fromfile(ddir / "dest.u8", np.uint8)
+        rows = np.fromfile(ddir / "batch_0.rows.u32", np.uint32)
+        off = np.fromfile(ddir / "batch_0.offsets.u64", np.uint64)
+        bounds = np.ascontiguousarray(off[np.arange(u + 1) * B])
+        router = ts.Router(exp["n_rows"], plan["dp_cut"], plan["flex_cut"], dest, u // w, w)
+        d_rows = torch.from_numpy(rows.view(np.int32)).cuda()
+        d_b = torch.from_numpy(bounds.view(np.int64)).cuda()
+        torch.cuda.synchronize()
+        kms, tms = [], []
+        for k in range(12):
+            counters = router.iteration_device(d_b.data_ptr(), d_rows.data_ptr(), rows.size)
+            if k >= 2:
+                km, tm = router.last_timing()
+                kms.append(km)
+                tms.append(tm)
+        router.close()
+        km, tm = float(np.median(kms)), float(np.median(tms))
+        algo = rows.size * 5
+        res[label] = {
+            "topology": f"{u // w} x {w}", "plan": plan["goal"], "dp_cut": plan["dp_cut"],
+            "flex_cut": plan["flex_cut"], "occurrences": int(rows.size),
+            "kernel_ms": round(km, 4), "iteration_ms": round(tm, 4),
+            "occurrences_per_s": round(rows.size / (km / 1e3), 1),
+            "algorithmic_bytes": algo, "hbm_gbs": round(algo / (km / 1e3) / 1e9, 1),
+            "hbm_frac": round(algo / (km / 1e3) / 1e9 / hbm, 4),
+            "bitmap_clear_bytes": int(u * ((exp["n_rows"] + 31) // 32) * 4),
+            "counters": counters.tolist(),
+            "_inputs": dict(dest=dest, rows=rows, bounds=bounds, u=u, w=w, plan=plan),
+        }
+        del d_rows, d_b
+    return res
+
+
 def run_ours(args, dist: Dist):
     import torch
     import paper_2301_02959_b200 as ts
@@ -299,6 +390,10 @@ def run_ours(args, dist: Dist):
         sampler = ts.Sampler(np.fromfile(data_dir / "alias.prob.f64", np.float64),
                              np.fromfile(data_dir / "alias.idx.u32", np.uint32), L, seed=7, device=device)
 
+    # NVLink ceiling of this box, measured in this run before any table
+    # exists: tools/p2p_bw's all-to-all row-store pattern (the serve /
+    # gradient-push access pattern), every GPU of the job at once
+    p2p_ceiling = dist.bcast(measure_p2p_ceiling(u) if (u > 1 and g == 0) else None) if u > 1 else None
     nccl_id = None
     if u > 1:
         nccl_id = dist.bcast(ts.nccl_unique_id() if g == 0 else None)
@@ -540,10 +635,18 @@ def run_ours(args, dist: Dist):
     ref_conv = {k: float(np.mean([t["reference_convention"][k] for t in tr]))
                 for k in tr[0]["reference_convention"]}
     off_dev = {k: float(np.mean([t["off_device"][k] for t in tr])) for k in tr[0]["off_device"]}
+    max_send = {k: float(np.mean([t["max_send_bytes"][k] for t in tr])) / 1e9 for k in tr[0]["max_send_bytes"]}
+    max_send_off = {k: float(np.mean([t["max_send_off_device_bytes"][k] for t in tr])) / 1e9
+                    for k in tr[0]["max_send_off_device_bytes"]}
     a2a = {
         "unit": "GB per iteration (one direction, one pass, whole job)",
         "saved_vs_rw_reference_convention": (ref_conv["rw_global_bytes"] - ref_conv["plan_global_bytes"]) / 1e9,
-        "saved_vs_tw_reference_convention": (ref_conv["tw_global_bytes"] - ref_conv["plan_global_bytes"]) / 1e9,
+        # table-wise moves the same total as row-wise under the reference's
+        # self-inclusive convention; where it differs is the most loaded
+        # server (one table = one GPU): the all-to-all's critical path
+        "max_send_per_gpu_GB": {"plan": max_send["plan"], "rw": max_send["rw"], "tw": max_send["tw"],
+                                "convention": "reference (self-inclusive)"},
+        "max_send_per_gpu_off_device_GB": max_send_off,
         "global_a2a_reduction": 1 - ref_conv["plan_global_bytes"] / ref_conv["rw_global_bytes"],
         "predicted_reduction": plan["predicted"]["global_a2a_reduction"],
         "saved_vs_rw_off_device": (off_dev["rw_bytes"] - off_dev["plan_global_bytes"] - off_dev["plan_intra_bytes"]) / 1e9,
@@ -568,10 +671,10 @@ def run_ours(args, dist: Dist):
         }
         total = sum(per_gpu.values())
         step_s = dev_ms / args.steps / 1e3
-        peer_peak = 770.0
+        peer_peak, peak_src = nvlink_peak(p2p_ceiling)
         nvlink = {"bytes_per_gpu_per_step": total, "breakdown": per_gpu,
                   "achieved_gbs": round(total / step_s / 1e9, 1), "peak_gbs": peer_peak,
-                  "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
+                  "peak_source": peak_src, "p2p_ceiling": p2p_ceiling,
                   "frac": round(total / step_s / 1e9 / peer_peak, 4),
                   "bound_ms": round(total / (peer_peak * 1e9) * 1e3, 4)}
 
@@ -586,11 +689,38 @@ def run_ours(args, dist: Dist):
     if u > 1:
         fwd_rows = (off_dev["plan_global_bytes"] + off_dev["plan_intra_bytes"]) / u
         lookup["nvlink_gbs_per_gpu"] = round(fwd_rows / (lookup_ms / 1e3) / 1e9, 1)
-        lookup["nvlink_frac"] = round(fwd_rows / (lookup_ms / 1e3) / 1e9 / 770.0, 4)
+        lookup["nvlink_frac"] = round(fwd_rows / (lookup_ms / 1e3) / 1e9 / nvlink_peak(p2p_ceiling)[0], 4)
+
+    # ---- routing at logical U = 8 (the reference loop's scale), N = 1 -------
+    routing = None
+    if u == 1 and not args.no_routing and g == 0:
+        routing = run_routing(args, dist)
+
+    # ---- parity of this run's path on one C2 batch (N = 1): a fresh table,
+    # one step on batch 0, every touched row read back for the oracle check
+    parity_dev = None
+    if u == 1 and not args.no_cpu_baseline and g == 0:
+        table.close()
+        table = ts.Table(n_rows=exp["n_rows"], dim=D, dp_cut=plan["dp_cut"], flex_cut=plan["flex_cut"],
+                         num_nodes=1, gpus_per_node=1, rank=0, device=device, weight_seed=1234, optimizer=opt,
+                         lr=args.lr, max_occurrences=max_occ)
+        b0 = d_rows[0]
+        table.train_step(b0.data_ptr(), b0.numel(), d_out.data_ptr())
+        table.synchronize()
+        probe = np.random.default_rng(5).choice(batches[0].size, size=min(100_000, batches[0].size), replace=False)
+        probe.sort()
+        out_probe = d_out[torch.from_numpy(probe).to(d_out.device)].cpu().numpy()
+        touched = np.unique(batches[0])
+        w_dev, st_dev = table.read_rows(touched, with_state=True)
+        parity_dev = dict(probe=probe, out_probe=out_probe, touched=touched, w=w_dev, state=st_dev,
+                          loss=table.loss())
 
     cpu = None
+    parity = None
     if dist.rank == 0 and u == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_port(batches[0], dest, plan, exp, B, D, args)
+        cpu, parity = cpu_baseline_port(batches[0], dest, plan, exp, B, D, args, parity_dev, routing)
+    for r in (routing or {}).values():
+        r.pop("_inputs", None)
 
     result = {
         "metric": METRIC,
@@ -610,18 +740,9 @@ def run_ours(args, dist: Dist):
                 ("synthetic: reference synthesize_zipf (seeds 1000+t); every step's batch drawn on the GPU "
                  "inside the timed region (ts_sampler: the Workload's per-sample law over its alias table); "
                  "weights seeded-hash init"),
-        "config": {
-            "workload": f"{'C2' if (args.tables, args.rows, args.seq_len) == (8, 10_000_000, 128) else 'custom'}: "
-                        f"{args.tables} tables x {args.rows} rows x D={D} fp32, seq len {args.seq_len}"
-                        f"/table, batch {B}/GPU, Zipf {args.exponent}",
-            "topology": f"{u // w} x {w}" + (" virtual nodes, paper bw" if args.virtual_nodes else " homogeneous"),
-            "plan": plan["goal"], "dp_cut": plan["dp_cut"], "flex_cut": plan["flex_cut"],
-            "global_batch": u * B, "seq_len": args.seq_len * args.tables,
-            "parallelism": f"row-sharded over {u} GPU(s): DP/Flex/RW tiers",
-            "optimizer": args.optimizer, "l2": "flushed (256 MiB write) between timed steps, outside events",
-            "batches_cycled": len(batches) if sampler is None else "gpu-sampled per step",
-            "occurrences_per_gpu_step": occ_mean if sampler is None else float(np.mean(sampled_occ)),
-        },
+        "config": job_config(args, u, w, plan["goal"], plan["dp_cut"], plan["flex_cut"]),
+        "run": {"batches_cycled": len(batches) if sampler is None else "gpu-sampled per step",
+                "occurrences_per_gpu_step": occ_mean if sampler is None else float(np.mean(sampled_occ))},
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk,
@@ -629,6 +750,8 @@ def run_ours(args, dist: Dist):
         "a2a": a2a,
         "nvlink": nvlink,
         "lookup_exchange": lookup,
+        "routing": routing,
+        "parity": parity,
         "loss_last_step": loss,
         "step_trace_ms": trace,
         **({"step_trace_ms_all_ranks": all_traces} if all_traces else {}),
@@ -641,12 +764,19 @@ def run_ours(args, dist: Dist):
     return result
 
 
-def cpu_baseline_port(rows, dest, plan, exp, B, D, args):
+def cpu_baseline_port(rows, dest, plan, exp, B, D, args, dev=None, routing=None):
     """Oracle port (oracle/restate.c) of one step on the host cores: the
     reference's routing loop restated (single thread, as the reference runs
     one iteration) + gather + dedup/segment-sum + row-wise Adagrad (threaded).
     Bounded sample: the first batch of the workload, weights compacted to the
-    rows it touches (same values: seeded by canonical index)."""
+    rows it touches (same values: seeded by canonical index).
+
+    The same oracle results are then the checker of this run's device path
+    (after every timed region): `dev` = a fresh table's forward + update on
+    that batch (probe of the output, every touched row and its Adagrad state)
+    must equal them bit for bit; `routing` = the logical-U=8 router counters,
+    checked against the restated reference loop over the same 33.6M
+    occurrences.  Returns (cpu_baseline, parity)."""
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_bind as orc
     n = exp["n_rows"]
@@ -663,6 +793,9 @@ def cpu_baseline_port(rows, dest, plan, exp, B, D, args):
     t_route = time.perf_counter() - t0
     uniq, compact = np.unique(rows, return_inverse=True)
     w = orc.init_rows(1234, uniq.astype(np.uint32), D, threads)
+    w0_probe = None
+    if dev is not None:
+        w0_probe = orc.gather(w, compact.astype(np.uint32)[dev["probe"]], threads)
     state = np.zeros(uniq.size, np.float32)
     compact = compact.astype(np.uint32)
     t0 = time.perf_counter()
@@ -670,10 +803,42 @@ def cpu_baseline_port(rows, dest, plan, exp, B, D, args):
     orc.backward_update(w, state, compact, out, orc.OPT_ROWWISE_ADAGRAD, args.lr, 1e-8, threads)
     t_value = time.perf_counter() - t0
     total = t_route + t_value
-    return {"value": round(B / total, 2), "unit": "samples/s", "cores": threads, "kind": "port",
-            "sample": f"one C2 batch ({B} samples, {rows.size} occurrences): restated reference routing "
-                      f"loop {t_route:.3f}s (1 thread) + gather/dedup/Adagrad {t_value:.3f}s "
-                      f"({threads} threads); weights compacted to the {uniq.size} touched rows"}
+    cpu = {"value": round(B / total, 2), "unit": "samples/s", "cores": threads, "kind": "port",
+           "sample": f"one C2 batch ({B} samples, {rows.size} occurrences): restated reference routing "
+                     f"loop {t_route:.3f}s (1 thread) + gather/dedup/Adagrad {t_value:.3f}s "
+                     f"({threads} threads); weights compacted to the {uniq.size} touched rows"}
+    parity = {}
+    if dev is not None and args.optimizer == "adagrad":
+        assert np.array_equal(dev["touched"], uniq)
+        parity["value_path"] = {
+            "what": "fresh table, one train step on C2 batch 0, vs oracle/restate.c (parity unpinned: the "
+                    "reference has no value path)",
+            "occurrences": int(rows.size), "touched_rows": int(uniq.size),
+            "forward_probe_occurrences": int(dev["probe"].size),
+            "forward_bit_exact": bool(np.array_equal(dev["out_probe"].view(np.uint32), w0_probe.view(np.uint32))),
+            "weights_bit_exact": bool(np.array_equal(dev["w"].view(np.uint32), w.view(np.uint32))),
+            "state_bit_exact": bool(np.array_equal(dev["state"].view(np.uint32), state.view(np.uint32))),
+            "weights_max_abs_diff": float(np.abs(dev["w"] - w).max()),
+        }
+    for label, r in (routing or {}).items():
+        inp = r.pop("_inputs")
+        n_r = inp["dest"].size
+        dp_r, fx_r = inp["plan"]["dp_cut"], inp["plan"]["flex_cut"]
+        idx = np.arange(n_r, dtype=np.uint64)
+        tier_r = np.where(idx < dp_r, 0, np.where(idx < fx_r, 1, 2)).astype(np.uint8)
+        del idx
+        owner_r = np.where(tier_r == 2, inp["dest"], 0).astype(np.uint32)
+        slot_r = np.where(tier_r == 1, inp["dest"], 0).astype(np.uint32)
+        t0 = time.perf_counter()
+        ref_c = orc.route_counts(inp["u"], inp["w"], 1, inp["bounds"], inp["rows"], tier_r, owner_r, slot_r)
+        t_r = time.perf_counter() - t0
+        r["cpu_port_occurrences_per_s_1thread"] = round(inp["rows"].size / t_r, 1)
+        parity[f"routing_{label}"] = {
+            "what": "GPU router counters (7 x U) vs the restated reference loop (oracle/restate.c, pinned to "
+                    "the reference's SimReport), one logical C2 iteration",
+            "occurrences": int(inp["rows"].size),
+            "bit_exact": bool(np.array_equal(np.array(r["counters"], np.uint64), ref_c))}
+    return cpu, (parity or None)
 
 
 # --------------------------------------------------------------------------
@@ -689,7 +854,11 @@ def run_reference(args, dist: Dist):
         return {"impl": "reference", "unavailable": "oracle/_ref/ref_driver was not built (needs /root/reference)"}
     spec = workload_spec(args, n_gpus)
     threads = max(1, min(len(os.sched_getaffinity(0)), args.steps, 32))
-    spec["workload"] = dict(seed=7, iterations=args.steps, materialize_pass=False)
+    # the reference's simulate() samples every iteration inside its timed
+    # pool; the same pool materializing alone (materialize_parallel) is
+    # subtracted so `value` is routing + accounting, like for like with the
+    # GPU arm, whose batches are materialized before its timed region
+    spec["workload"] = dict(seed=7, iterations=args.steps, materialize_pass=False, materialize_parallel=True)
     spec["threads"] = threads
     spec["simulate"] = True
     spec["frontier"] = False
@@ -701,9 +870,12 @@ def run_reference(args, dist: Dist):
     doc = json.loads((tmp / "out.json").read_text())
     wall = time.time() - t0
     sim_s = doc["timing"]["simulate_s"]
+    sample_s = doc["timing"]["materialize_parallel_s"]
+    route_s = max(sim_s - sample_s, 1e-9)
     u = spec["topology"]["num_nodes"] * spec["topology"]["gpus_per_node"]
+    w = spec["topology"]["gpus_per_node"]
     samples = args.steps * u * args.batch
-    value = samples / sim_s
+    value = samples / route_s
     return {
         "impl": "reference",
         "metric": METRIC,
@@ -712,21 +884,20 @@ def run_reference(args, dist: Dist):
         "n_gpus": n_gpus,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": round(1e3 * sim_s / args.steps, 3),
+        "ms_per_step": round(1e3 * route_s / args.steps, 3),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64 (integer routing + fp64 accounting)",
         "data": "synthetic (same workload as --impl ours)",
-        "config": {"workload": f"C2: {args.tables} tables x {args.rows} rows x D={args.dim}, seq len "
-                               f"{args.seq_len}/table, batch {args.batch}/GPU, Zipf {args.exponent}",
-                   "topology": f"{spec['topology']['num_nodes']} x {spec['topology']['gpus_per_node']}",
-                   "plan": spec["goal"]},
+        "config": job_config(args, u, w, doc["plan"]["goal"], doc["plan"]["dp_cut"], doc["plan"]["flex_cut"]),
         "cpu_baseline": {"value": round(value, 2), "unit": "samples/s", "cores": threads, "kind": "reference",
                          "sample": f"tiershard::simulate (unmodified reference, oracle/_ref) over {args.steps} "
-                                   f"iterations of the workload, threads={threads}: its stock path samples each "
-                                   "iteration and routes/counts every occurrence; the reference has no "
+                                   f"iterations of the workload, threads={threads}, minus the same pool's "
+                                   f"Workload::materialize_iteration time ({sample_s:.2f} of {sim_s:.2f} s): "
+                                   "routing + traffic accounting of every occurrence; the reference has no "
                                    "gather/exchange/update to time"},
+        "value_including_sampling": round(samples / sim_s, 2),
         "e2e": {"value": round(value, 2), "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "reference_timing": doc["timing"],
         "wall_s": round(wall, 1),

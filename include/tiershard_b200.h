@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 1
+#define TS_ABI_VERSION 2
 
 typedef enum ts_status {
   TS_OK = 0,
@@ -109,6 +109,11 @@ ts_status ts_router_iteration(ts_router* r, uint32_t local_batch,
 ts_status ts_router_iteration_device(ts_router* r, const uint64_t* d_requester_begin,
                                      const uint32_t* d_rows, uint64_t occurrences,
                                      uint64_t* counters);
+
+/* Device time of the last iteration (CUDA events on the router's stream):
+ * the routing kernel alone, and the whole iteration including the counter /
+ * distinct-bitmap clears (U x n_rows bits). */
+ts_status ts_router_last_timing(ts_router* r, double* kernel_ms, double* total_ms);
 
 ts_status ts_router_destroy(ts_router* r);
 
@@ -232,6 +237,19 @@ ts_status ts_exchange_plan(uint32_t num_nodes, uint32_t gpus_per_node, uint32_t 
  * ---------------------------------------------------------------------- */
 typedef struct ts_table ts_table;
 
+/* In-process rank group: all U ranks of a job are host threads of ONE process
+ * (any mix of GPUs, including several ranks on one GPU, which NCCL cannot
+ * do).  Passed as ts_table_config.group instead of an NCCL id, it carries the
+ * table's collectives (host all-gather, device rendezvous by cross-stream
+ * events) and maps peer buffers by plain device pointers; the exchange is
+ * the peer-memory path.  Each rank's table must be created, stepped and
+ * destroyed by its own thread, collectively (a rendezvous that does not
+ * complete within TIERSHARD_GROUP_TIMEOUT seconds, default 300, fails the
+ * call and poisons the group).  Destroy the group after its tables. */
+typedef struct ts_group ts_group;
+ts_status ts_group_create(ts_group** out, uint32_t ranks);
+ts_status ts_group_destroy(ts_group* g);
+
 typedef struct ts_table_config {
   uint32_t num_nodes;      /* N */
   uint32_t gpus_per_node;  /* W */
@@ -246,7 +264,9 @@ typedef struct ts_table_config {
   float lr;
   float eps;               /* Adagrad epsilon */
   uint64_t max_occurrences;      /* capacity: occurrences per step, this rank */
-  const void* nccl_unique_id;    /* 128-byte ncclUniqueId; NULL iff N*W == 1 */
+  const void* nccl_unique_id;    /* 128-byte ncclUniqueId (one process per rank) */
+  struct ts_group* group;        /* in-process rank group (ts_group_create), or NULL;
+                                    U > 1 needs exactly one of nccl_unique_id / group */
 } ts_table_config;
 
 /* Collective over all U ranks when U > 1 (NCCL communicator creation). */
@@ -301,6 +321,11 @@ ts_status ts_table_counters(ts_table* t, uint64_t* counters);
 ts_status ts_table_read_rows(ts_table* t, const uint32_t* rows, uint64_t count,
                              float* h_weights, float* h_state);
 
+/* Waits for this rank's queued work.  With U > 1 on the peer-memory path it
+ * is COLLECTIVE (every rank calls it): peers store into this rank's
+ * replicated rows and receive buffers, so it first rendezvous with them and
+ * returns once every rank's queued steps are complete -- after it,
+ * ts_table_read_rows sees the final replicated rows. */
 ts_status ts_table_synchronize(ts_table* t);
 
 /* Per-phase device time accumulated since the last reset (CUDA events on the

@@ -20,6 +20,7 @@
 // (paper_2301_02959_b200 ts_driver) accepts the same spec and emits the same
 // keys so the tests can compare the two documents field by field.
 
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -307,6 +308,29 @@ json run(const json& spec) {
     }
     timing["materialize_total_s_1thread"] = now_s() - t0;
     out["occurrences"] = occ;
+  }
+
+  if (jw.value("materialize_parallel", false)) {
+    // the sampling share of simulate(): every iteration materialized by the
+    // same number of threads pulling iterations from an atomic counter, the
+    // way simulate()'s pool does (simulator.cpp:336-364), without routing --
+    // bench.py subtracts it to time routing + accounting alone
+    std::atomic<uint32_t> next{0};
+    std::atomic<uint64_t> occ_sum{0};
+    t0 = now_s();
+    std::vector<std::thread> pool;
+    for (unsigned k = 0; k < threads; ++k) {
+      pool.emplace_back([&] {
+        ts::IterationBatch batch;
+        for (uint32_t it = next++; it < iters; it = next++) {
+          wl.materialize_iteration(it, batch);
+          occ_sum += batch.occurrences();
+        }
+      });
+    }
+    for (auto& th : pool) th.join();
+    timing["materialize_parallel_s"] = now_s() - t0;
+    timing["materialize_parallel_occurrences"] = occ_sum.load();
   }
 
   if (spec.value("simulate", true)) {

@@ -14,6 +14,7 @@ from .capi import (  # noqa: F401
     KeyMap,
     Sampler,
     Table,
+    Group,
     load,
     build_info,
     device_count,

@@ -50,6 +50,7 @@ EXPORTS = (
     "ts_router_iteration",
     "ts_router_iteration_device",
     "ts_router_destroy",
+    "ts_router_last_timing",
     "ts_shard_layout",
     "ts_exchange_plan",
     "ts_table_create",
@@ -77,6 +78,8 @@ EXPORTS = (
     "ts_sampler_destroy",
     "ts_table_train_steps_host",
     "ts_frontier_preview",
+    "ts_group_create",
+    "ts_group_destroy",
 )
 
 
@@ -104,6 +107,7 @@ class TableConfig(C.Structure):
         ("eps", C.c_float),
         ("max_occurrences", C.c_uint64),
         ("nccl_unique_id", C.c_void_p),
+        ("group", C.c_void_p),
     ]
 
 
@@ -139,6 +143,7 @@ def load() -> C.CDLL:
         "ts_router_iteration": (C.c_int, [vp, C.c_uint32, vp, vp, C.c_uint64, vp]),
         "ts_router_iteration_device": (C.c_int, [vp, vp, vp, C.c_uint64, vp]),
         "ts_router_destroy": (C.c_int, [vp]),
+        "ts_router_last_timing": (C.c_int, [vp, f64p, f64p]),
         "ts_shard_layout": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, vp, C.c_uint32, C.c_uint32,
                                       C.c_uint32, vp, u64p, u64p, u64p]),
         "ts_exchange_plan": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, vp, vp, vp, vp, vp, u64p,
@@ -168,6 +173,8 @@ def load() -> C.CDLL:
         "ts_sampler_destroy": (C.c_int, [vp]),
         "ts_table_train_steps_host": (C.c_int, [vp, vp, vp, C.c_uint32, vp]),
         "ts_frontier_preview": (C.c_int, [C.c_int, C.c_uint64, vp, C.c_uint32, vp, vp]),
+        "ts_group_create": (C.c_int, [C.POINTER(vp), C.c_uint32]),
+        "ts_group_destroy": (C.c_int, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -254,6 +261,20 @@ class Router:
                                              _ptr(r) if r.size else None, r.size, _ptr(out)))
         return out.reshape(7, self.u)
 
+    def iteration_device(self, d_requester_begin: int, d_rows: int, occurrences: int) -> np.ndarray:
+        """Device-resident iteration: U+1 u64 requester bounds and the rows
+        (device pointers); counters to host."""
+        out = np.zeros(7 * self.u, dtype=np.uint64)
+        _check(self._lib.ts_router_iteration_device(self._h, d_requester_begin, d_rows or None, occurrences,
+                                                    _ptr(out)))
+        return out.reshape(7, self.u)
+
+    def last_timing(self) -> tuple[float, float]:
+        """(kernel ms, whole-iteration ms incl. clears) of the last iteration."""
+        k, t = C.c_double(), C.c_double()
+        _check(self._lib.ts_router_last_timing(self._h, C.byref(k), C.byref(t)))
+        return k.value, t.value
+
     def close(self):
         if getattr(self, "_h", None):
             _check(self._lib.ts_router_destroy(self._h))
@@ -334,6 +355,36 @@ class Sampler:
             pass
 
 
+class Group:
+    """ts_group_*: the in-process rank group.  Every rank of a U-rank job is a
+    host thread of this process (any GPUs, several ranks per GPU allowed);
+    pass the group to each rank's Table instead of an NCCL id, and create,
+    step and close each Table from its own thread (ctypes releases the GIL
+    during the calls, so the ranks' collectives meet)."""
+
+    def __init__(self, ranks: int):
+        self._lib = load()
+        h = vp()
+        _check(self._lib.ts_group_create(C.byref(h), ranks))
+        self._h = h
+        self.ranks = ranks
+
+    @property
+    def handle(self) -> int:
+        return self._h.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _check(self._lib.ts_group_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Table:
     """ts_table_*: one rank's shard with lookup (forward) and update (backward)."""
 
@@ -342,12 +393,15 @@ class Table:
                  gpus_per_node: int = 1, rank: int = 0, device: int = 0,
                  weight_seed: int = 1234, optimizer: int = OPT_SGD, lr: float = 0.01,
                  eps: float = 1e-8, max_occurrences: int = 1 << 20,
-                 nccl_unique_id: bytes | None = None):
+                 nccl_unique_id: bytes | None = None, group: Group | None = None):
         self._lib = load()
         self.u = num_nodes * gpus_per_node
         self.dim = dim
         cfg = TableConfig(num_nodes, gpus_per_node, rank, device, dim, n_rows, dp_cut, flex_cut,
-                          weight_seed, optimizer, lr, eps, max_occurrences, None)
+                          weight_seed, optimizer, lr, eps, max_occurrences, None, None)
+        if group is not None:
+            cfg.group = group.handle
+            self._group = group  # outlives the table
         self._id_buf = None
         if nccl_unique_id is not None:
             self._id_buf = C.create_string_buffer(nccl_unique_id, len(nccl_unique_id))

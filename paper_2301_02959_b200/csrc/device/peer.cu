@@ -234,7 +234,15 @@ IpcExport export_pointer(const void* ptr) {
   return e;
 }
 
+IpcExport direct_export(const void* ptr) {
+  IpcExport e;
+  std::memset(&e, 0, sizeof(e));
+  e.base_id = reinterpret_cast<uint64_t>(ptr);
+  return e;
+}
+
 void* PeerMappings::open(int peer, const IpcExport& e) {
+  if (direct_) return reinterpret_cast<char*>(e.base_id) + e.offset;
   // keyed by base address, validated by handle: an exporter that freed and
   // re-allocated at the same address sends a different handle, and the stale
   // mapping is replaced instead of reused

@@ -36,6 +36,9 @@ static_assert(sizeof(IpcExport) == 80, "IpcExport is part of the all-gather payl
 
 // Export of the allocation containing `ptr`.
 IpcExport export_pointer(const void* ptr);
+// In-process export (ranks that are threads of one process, group.cuh): the
+// raw device address; PeerMappings in direct mode hands it back unchanged.
+IpcExport direct_export(const void* ptr);
 
 // Per-peer cache of opened IPC allocations.
 class PeerMappings {
@@ -43,6 +46,8 @@ class PeerMappings {
   // Device pointer (valid in this process) for a peer's export.
   void* open(int peer, const IpcExport& e);
   void close_all();
+  void set_direct(bool direct) { direct_ = direct; }
+  bool direct() const { return direct_; }
   ~PeerMappings() { close_all(); }
 
  private:
@@ -52,6 +57,7 @@ class PeerMappings {
   };
   std::map<std::pair<int, uint64_t>, Mapping> opened_;  // (peer, base_id) -> mapping
   uint64_t opens_ = 0, reopens_ = 0;
+  bool direct_ = false;
 };
 
 // Request lists a server pulls: for each source rank, a run of `count`

@@ -40,6 +40,7 @@
 
 #include "common.cuh"
 #include "embedding.cuh"
+#include "group.cuh"
 #include "primitives.cuh"
 #include "layout.hpp"
 #include "peer.cuh"
@@ -100,6 +101,46 @@ enum Phase : int {
   kNumPhases
 };
 
+// In-process staged path (group transport): out[i] = sum of the group's
+// buffers in group-rank order, the stand-in for ncclAllReduce.
+struct SumSources {
+  const float* src[kMaxPeerRanks];
+  int n;
+};
+__global__ void sum_sources_kernel(float* __restrict__ out, SumSources s, uint64_t count) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
+    float v = s.src[0][i];
+    for (int k = 1; k < s.n; ++k) v = __fadd_rn(v, s.src[k][i]);
+    out[i] = v;
+  }
+}
+
+__global__ void gather_scalars_kernel(const float* __restrict__ src, const uint32_t* __restrict__ idx,
+                                      float* __restrict__ dst, uint64_t count) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
+    dst[i] = src[idx[i]];
+  }
+}
+
+// U = 1 tier counts of a batch (RW, Flex, DP), for ts_table_counters: the
+// forward does not bucket at U = 1, so they are counted on demand.
+__global__ void count_tiers_kernel(const uint32_t* __restrict__ rows, uint64_t occ, uint64_t dp_cut,
+                                   uint64_t flex_cut, unsigned long long* __restrict__ tiers) {
+  unsigned long long c[3] = {0, 0, 0};
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < occ; i += stride) {
+    const uint32_t r = rows[i];
+    c[r < dp_cut ? 2 : (r < flex_cut ? 1 : 0)] += 1;
+  }
+  for (int k = 0; k < 3; ++k) {
+    unsigned long long v = c[k];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if ((threadIdx.x & 31u) == 0 && v) atomicAdd(tiers + k, v);
+  }
+}
+
 const char* const kPhaseNames[kNumPhases] = {
     "route",         "gather",         "exchange_fwd", "scatter",  "exchange_bwd",
     "dedup_sort",    "segment_starts", "segment_update", "allreduce", "dense_update",
@@ -143,6 +184,14 @@ struct ts_table {
   cudaEvent_t ev_ids = nullptr, ev_fwd = nullptr, ev_bwd0 = nullptr, ev_grads = nullptr,
               ev_dense = nullptr, ev_ar = nullptr;
   ncclComm_t world = nullptr, intra = nullptr, cross = nullptr;
+  // in-process group transport (cfg.group): replaces the NCCL communicators
+  // for the peer-memory path (group.cuh); `ready` = creation completed, so
+  // destroy() may run its collective rendezvous
+  ts_group* grp = nullptr;
+  bool attached = false, ready = false;
+  tsd::IpcExport export_ptr(const void* p) const {
+    return grp ? tsd::direct_export(p) : tsd::export_pointer(p);
+  }
 
   // shard
   uint64_t local_rows = 0, dp_rows = 0, flex_rows = 0, rw_rows = 0;
@@ -218,6 +267,10 @@ struct ts_table {
   std::vector<uint8_t> allgather_bytes(const void* mine, size_t bytes);
   void barrier_on_comm();
   void setup_p2p();
+  // staged path over the in-process group: sum of `count` floats of `buf`
+  // over the group's members (ranks `members`, in order), in place
+  tsd::DevBuf<float> ar_tmp;
+  void group_allreduce(float* buf, uint64_t count, const std::vector<uint32_t>& members, cudaStream_t on);
   void forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out);
   void backward_p2p(const float* d_grad);
 
@@ -356,7 +409,10 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
   if (c.max_occurrences == 0 || c.max_occurrences >= 0x7FFFFFFFull) {
     fail(TS_ERR_CONFIG, "table: max_occurrences must be in [1, 2^31)");
   }
-  if (U > 1 && !c.nccl_unique_id) fail(TS_ERR_CONFIG, "table: U > 1 needs an NCCL unique id");
+  if (U > 1 && !c.nccl_unique_id && !c.group) {
+    fail(TS_ERR_CONFIG, "table: U > 1 needs an NCCL unique id or an in-process group");
+  }
+  if (c.group && tsd::group_size(c.group) != U) fail(TS_ERR_CONFIG, "table: group size differs from N*W");
   if (U > 1 && !tier_dest) fail(TS_ERR_CONFIG, "table: U > 1 needs the placement table");
   use_device(c.device);
   TSD_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
@@ -495,11 +551,17 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     for (cudaEvent_t* e : {&ev_ids, &ev_fwd, &ev_bwd0, &ev_grads, &ev_dense, &ev_ar}) {
       TSD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
-    ncclUniqueId id;
-    std::memcpy(&id, c.nccl_unique_id, sizeof(id));
-    TSD_NCCL(ncclCommInitRank(&world, static_cast<int>(U), id, static_cast<int>(g)));
-    TSD_NCCL(ncclCommSplit(world, static_cast<int>(node), static_cast<int>(g), &intra, nullptr));
-    TSD_NCCL(ncclCommSplit(world, static_cast<int>(slot), static_cast<int>(g), &cross, nullptr));
+    if (c.group) {
+      grp = c.group;
+      group_attach(grp, g, c.device);
+      attached = true;
+    } else {
+      ncclUniqueId id;
+      std::memcpy(&id, c.nccl_unique_id, sizeof(id));
+      TSD_NCCL(ncclCommInitRank(&world, static_cast<int>(U), id, static_cast<int>(g)));
+      TSD_NCCL(ncclCommSplit(world, static_cast<int>(node), static_cast<int>(g), &intra, nullptr));
+      TSD_NCCL(ncclCommSplit(world, static_cast<int>(slot), static_cast<int>(g), &cross, nullptr));
+    }
     setup_p2p();
   }
 }
@@ -508,10 +570,14 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
 // Collective on the comm stream; synchronises it.
 std::vector<uint8_t> ts_table::allgather_bytes(const void* mine, size_t bytes) {
   using namespace tsd;
+  std::vector<uint8_t> all(bytes * U);
+  if (grp) {
+    group_allgather(grp, g, mine, bytes, all.data());
+    return all;
+  }
   xfer.ensure(bytes * U);
   TSD_CUDA(cudaMemcpyAsync(xfer.ptr + bytes * g, mine, bytes, cudaMemcpyHostToDevice, comm));
   TSD_NCCL(ncclAllGather(xfer.ptr + bytes * g, xfer.ptr, bytes, ncclUint8, world, comm));
-  std::vector<uint8_t> all(bytes * U);
   TSD_CUDA(cudaMemcpyAsync(all.data(), xfer.ptr, bytes * U, cudaMemcpyDeviceToHost, comm));
   TSD_CUDA(cudaStreamSynchronize(comm));
   return all;
@@ -521,6 +587,10 @@ std::vector<uint8_t> ts_table::allgather_bytes(const void* mine, size_t bytes) {
 // work queued before it on every rank completes before work queued after it.
 void ts_table::barrier_on_comm() {
   using namespace tsd;
+  if (grp) {
+    group_barrier(grp, g, comm);
+    return;
+  }
   TSD_NCCL(ncclAllReduce(barrier_buf.ptr, barrier_buf.ptr, 1, ncclInt32, ncclSum, world, comm));
 }
 
@@ -535,10 +605,36 @@ void ts_table::setup_p2p() {
   if (const char* env = std::getenv("TIERSHARD_EXCHANGE")) {
     if (std::string(env) == "nccl") ok = 0;
   }
+  if (grp) {
+    // in-process ranks: the peer-memory path is the only one (no NCCL);
+    // ranks on other GPUs of this process are reached by UVA pointers
+    if (U > kMaxPeerRanks) fail(TS_ERR_CONFIG, "table: the in-process group supports U <= 8");
+    int32_t dev = cfg.device;
+    const std::vector<uint8_t> devs = allgather_bytes(&dev, sizeof(dev));
+    for (uint32_t p = 0; p < U; ++p) {
+      int32_t pd;
+      std::memcpy(&pd, devs.data() + sizeof(pd) * p, sizeof(pd));
+      if (pd == cfg.device) continue;
+      int can = 0;
+      TSD_CUDA(cudaDeviceCanAccessPeer(&can, cfg.device, pd));
+      if (!can) fail(TS_ERR_CONFIG, "table: in-process group ranks on GPUs without peer access");
+      const cudaError_t e = cudaDeviceEnablePeerAccess(pd, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else {
+        TSD_CUDA(e);
+      }
+    }
+    peers.set_direct(true);
+    if (!ok) {  // TIERSHARD_EXCHANGE=nccl: the staged path, its collectives over the group
+      p2p = false;
+      return;
+    }
+  }
   char bus[32] = {};
   TSD_CUDA(cudaDeviceGetPCIBusId(bus, sizeof(bus), cfg.device));
   const std::vector<uint8_t> buses = allgather_bytes(bus, sizeof(bus));
-  for (uint32_t p = 0; p < U && ok; ++p) {
+  for (uint32_t p = 0; p < U && ok && !grp; ++p) {
     if (p == g) continue;
     int dev = -1, can = 0;
     if (cudaDeviceGetByPCIBusId(&dev, reinterpret_cast<const char*>(buses.data() + sizeof(bus) * p)) !=
@@ -562,17 +658,17 @@ void ts_table::setup_p2p() {
   if (const char* env = std::getenv("TIERSHARD_GRADS")) grads_push = std::string(env) != "pull";
   if (const char* env = std::getenv("TIERSHARD_PUSH_ORDER")) push_first = std::string(env) == "first";
   // export the table-owned buffers peers read or write
-  auto exp_or_none = [](const void* p) {
+  auto exp_or_none = [this](const void* p) {
     IpcExport e;
     std::memset(&e, 0, sizeof(e));
-    return p ? export_pointer(p) : e;
+    return p ? (grp ? direct_export(p) : export_pointer(p)) : e;
   };
   constexpr int kExports = 10;
-  IpcExport mine[kExports] = {export_pointer(send_ids.ptr), export_pointer(order.ptr),
-                              export_pointer(loss_partials.ptr + gather_grid), exp_or_none(dense_dp.ptr),
-                              export_pointer(d_w), exp_or_none(d_state), exp_or_none(dense_flex.ptr),
+  IpcExport mine[kExports] = {export_ptr(send_ids.ptr), export_ptr(order.ptr),
+                              export_ptr(loss_partials.ptr + gather_grid), exp_or_none(dense_dp.ptr),
+                              export_ptr(d_w), exp_or_none(d_state), exp_or_none(dense_flex.ptr),
                               exp_or_none(stamp_dp.ptr), exp_or_none(stamp_flex.ptr),
-                              export_pointer(recv_rows.ptr)};
+                              export_ptr(recv_rows.ptr)};
   const std::vector<uint8_t> all = allgather_bytes(mine, sizeof(mine));
   peer_ids.assign(U, nullptr);
   peer_pos.assign(U, nullptr);
@@ -615,6 +711,25 @@ void ts_table::setup_p2p() {
 // The per-peer buffers are laid out [peer p: RW part | Flex part].
 // ---------------------------------------------------------------------------
 
+void ts_table::group_allreduce(float* buf, uint64_t count, const std::vector<uint32_t>& members,
+                               cudaStream_t on) {
+  using namespace tsd;
+  const uint64_t mine = reinterpret_cast<uint64_t>(buf);
+  std::vector<uint64_t> all(U);
+  group_allgather(grp, g, &mine, sizeof(mine), all.data());
+  ar_tmp.ensure(count);
+  SumSources ss{};
+  for (uint32_t p : members) ss.src[ss.n++] = reinterpret_cast<const float*>(all[p]);
+  group_barrier(grp, g, on);  // every member's partial sums are complete
+  if (count) {
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((count + 255) / 256, 4u * sm_count()));
+    sum_sources_kernel<<<grid, 256, 0, on>>>(ar_tmp.ptr, ss, count);
+    TSD_LAUNCH_CHECK();
+  }
+  group_barrier(grp, g, on);  // every member has read every buffer
+  if (count) TSD_CUDA(cudaMemcpyAsync(buf, ar_tmp.ptr, sizeof(float) * count, cudaMemcpyDeviceToDevice, on));
+}
+
 void ts_table::exchange(const void* send, const std::vector<uint64_t>& s_off,
                         const std::vector<uint64_t>& s_cnt, void* recv,
                         const std::vector<uint64_t>& r_off, const std::vector<uint64_t>& r_cnt,
@@ -622,6 +737,31 @@ void ts_table::exchange(const void* send, const std::vector<uint64_t>& s_off,
   // s_off/s_cnt/r_off/r_cnt have 2*U entries: [p*2 + 0] RW, [p*2 + 1] Flex.
   auto* sb = static_cast<const char*>(send);
   auto* rb = static_cast<char*>(recv);
+  if (grp) {
+    // in-process: every rank's send base + offsets, a device rendezvous (the
+    // send data is complete everywhere), each receiver copies its runs out
+    // of the senders' buffers, a rendezvous (the senders may reuse them)
+    std::vector<uint64_t> mine(2 * U + 1);
+    mine[0] = reinterpret_cast<uint64_t>(sb);
+    std::copy(s_off.begin(), s_off.begin() + 2 * U, mine.begin() + 1);
+    std::vector<uint64_t> all(mine.size() * U);
+    tsd::group_allgather(grp, g, mine.data(), sizeof(uint64_t) * mine.size(), all.data());
+    tsd::group_barrier(grp, g, on);
+    for (uint32_t p = 0; p < U; ++p) {
+      if (p == g) continue;
+      const uint64_t* theirs = all.data() + mine.size() * p;
+      const char* base = reinterpret_cast<const char*>(theirs[0]);
+      for (int part = 0; part < 2; ++part) {
+        const uint64_t cnt = r_cnt[2 * p + part];
+        if (!cnt) continue;
+        TSD_CUDA(cudaMemcpyAsync(rb + r_off[2 * p + part] * elem_bytes,
+                                 base + theirs[1 + 2 * g + part] * elem_bytes, cnt * elem_bytes,
+                                 cudaMemcpyDefault, on));
+      }
+    }
+    tsd::group_barrier(grp, g, on);
+    return;
+  }
   TSD_NCCL(ncclGroupStart());
   for (uint32_t p = 0; p < U; ++p) {
     if (p == g) continue;
@@ -687,6 +827,13 @@ void ts_table::dedup_p2p(cudaStream_t on) {
 void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   using namespace tsd;
   if (occ > cfg.max_occurrences) fail(TS_ERR_VALIDATION, "table: batch exceeds max_occurrences");
+  // a forward not followed by a backward (eval, or forward twice) leaves
+  // the prefetched dedup running on aux over the shared sort buffers and
+  // request lists: this forward's route must not touch them before it ends
+  if (dedup_ready) {
+    TSD_CUDA(cudaStreamWaitEvent(stream, ev_dedup, 0));
+    dedup_ready = false;
+  }
   last_rows = d_rows;
   last_occ = occ;
   last_out = d_out;
@@ -748,11 +895,19 @@ void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
     // every NCCL call of this table is issued on the comm stream
     TSD_CUDA(cudaEventRecord(ev_ids, stream));
     TSD_CUDA(cudaStreamWaitEvent(comm, ev_ids, 0));
-    TSD_NCCL(ncclAllGather(bucket_start.ptr, all_counts.ptr, nb() + 1, ncclUint32, world, comm));
     h_counts.resize(static_cast<size_t>(U) * (nb() + 1));
-    TSD_CUDA(cudaMemcpyAsync(h_counts.data(), all_counts.ptr, sizeof(uint32_t) * U * (nb() + 1),
-                             cudaMemcpyDeviceToHost, comm));
-    TSD_CUDA(cudaStreamSynchronize(comm));
+    if (grp) {
+      std::vector<uint32_t> mine(nb() + 1);
+      TSD_CUDA(cudaMemcpyAsync(mine.data(), bucket_start.ptr, sizeof(uint32_t) * (nb() + 1),
+                               cudaMemcpyDeviceToHost, comm));
+      TSD_CUDA(cudaStreamSynchronize(comm));
+      group_allgather(grp, g, mine.data(), sizeof(uint32_t) * (nb() + 1), h_counts.data());
+    } else {
+      TSD_NCCL(ncclAllGather(bucket_start.ptr, all_counts.ptr, nb() + 1, ncclUint32, world, comm));
+      TSD_CUDA(cudaMemcpyAsync(h_counts.data(), all_counts.ptr, sizeof(uint32_t) * U * (nb() + 1),
+                               cudaMemcpyDeviceToHost, comm));
+      TSD_CUDA(cudaStreamSynchronize(comm));
+    }
   }
   // Send layout: my remote buckets are contiguous in bucket order (RW by
   // server, then Flex by slot); receive layout is ordered by source rank
@@ -930,15 +1085,24 @@ void ts_table::backward(const float* d_grad) {
   TSD_CUDA(cudaEventRecord(ev_dense, stream));
   TSD_CUDA(cudaStreamWaitEvent(comm, ev_dense, 0));
   t = phase_begin(kPhaseAllReduce, comm);
-  TSD_NCCL(ncclGroupStart());
-  if (dp_rows) {
-    TSD_NCCL(ncclAllReduce(dense_dp.ptr, dense_dp.ptr, dp_rows * cfg.dim, ncclFloat32, ncclSum, world, comm));
+  if (grp) {
+    // every rank calls both (collective), in the NCCL path's order
+    std::vector<uint32_t> world_ranks(U), cross_ranks(N);
+    for (uint32_t p = 0; p < U; ++p) world_ranks[p] = p;
+    for (uint32_t k = 0; k < N; ++k) cross_ranks[k] = k * W + slot;
+    group_allreduce(dense_dp.ptr, dp_rows * cfg.dim, world_ranks, comm);
+    if (N > 1) group_allreduce(dense_flex.ptr, flex_rows * cfg.dim, cross_ranks, comm);
+  } else {
+    TSD_NCCL(ncclGroupStart());
+    if (dp_rows) {
+      TSD_NCCL(ncclAllReduce(dense_dp.ptr, dense_dp.ptr, dp_rows * cfg.dim, ncclFloat32, ncclSum, world, comm));
+    }
+    if (N > 1 && flex_rows) {
+      TSD_NCCL(ncclAllReduce(dense_flex.ptr, dense_flex.ptr, flex_rows * cfg.dim, ncclFloat32, ncclSum,
+                             cross, comm));
+    }
+    TSD_NCCL(ncclGroupEnd());
   }
-  if (N > 1 && flex_rows) {
-    TSD_NCCL(ncclAllReduce(dense_flex.ptr, dense_flex.ptr, flex_rows * cfg.dim, ncclFloat32, ncclSum,
-                           cross, comm));
-  }
-  TSD_NCCL(ncclGroupEnd());
   phase_end(t);
   TSD_CUDA(cudaEventRecord(ev_ar, comm));
 
@@ -993,7 +1157,7 @@ void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   launch_bucket_starts(goff.ptr, 1, nb(), static_cast<uint32_t>(occ), my_starts, stream);
   // ids of the remote prefix (the local bucket is last; its count is on the device)
   launch_remote_ids_upto(d_rows, order.ptr, occ, my_starts + (U + W), d_local, send_ids.ptr, stream);
-  my_export = export_pointer(d_out);
+  my_export = export_ptr(d_out);
   TSD_CUDA(cudaMemcpyAsync(my_slot + starts_bytes, &my_export, sizeof(IpcExport), cudaMemcpyHostToDevice,
                            stream));
   phase_end(t);
@@ -1002,10 +1166,21 @@ void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   // (also the rendezvous after which peers may read our request lists)
   TSD_CUDA(cudaEventRecord(ev_ids, stream));
   TSD_CUDA(cudaStreamWaitEvent(comm, ev_ids, 0));
-  TSD_NCCL(ncclAllGather(my_slot, xfer.ptr, P, ncclUint8, world, comm));
   h_xfer.resize(P * U);
-  TSD_CUDA(cudaMemcpyAsync(h_xfer.data(), xfer.ptr, P * U, cudaMemcpyDeviceToHost, comm));
-  TSD_CUDA(cudaStreamSynchronize(comm));
+  if (grp) {
+    // in-process: this rank's slot to the host, then a host all-gather.
+    // Every rank synchronised its comm stream (which waited for the route)
+    // before the gather, so the request lists are complete before any pull
+    // -- at least the ordering the NCCL all-gather gives
+    std::vector<uint8_t> mine(P);
+    TSD_CUDA(cudaMemcpyAsync(mine.data(), my_slot, P, cudaMemcpyDeviceToHost, comm));
+    TSD_CUDA(cudaStreamSynchronize(comm));
+    group_allgather(grp, g, mine.data(), P, h_xfer.data());
+  } else {
+    TSD_NCCL(ncclAllGather(my_slot, xfer.ptr, P, ncclUint8, world, comm));
+    TSD_CUDA(cudaMemcpyAsync(h_xfer.data(), xfer.ptr, P * U, cudaMemcpyDeviceToHost, comm));
+    TSD_CUDA(cudaStreamSynchronize(comm));
+  }
   h_counts.resize(static_cast<size_t>(U) * (nb() + 1));
   std::vector<float*> peer_out(U, nullptr);
   for (uint32_t p = 0; p < U; ++p) {
@@ -1190,7 +1365,7 @@ void ts_table::backward_p2p(const float* d_grad) {
       }
       barrier_on_comm();  // every requester's rows have landed in every server
     } else {
-      const IpcExport mine = export_pointer(d_grad);
+      const IpcExport mine = export_ptr(d_grad);
       const std::vector<uint8_t> all = allgather_bytes(&mine, sizeof(mine));
       PullGrads pg{};
       for (uint32_t p = 0; p < U; ++p) {
@@ -1315,7 +1490,24 @@ void ts_table::backward_p2p(const float* d_grad) {
 void ts_table::destroy() {
   cudaSetDevice(cfg.device);
   if (stream) cudaStreamSynchronize(stream);
+  if (aux) cudaStreamSynchronize(aux);
+  if (ready && p2p) {
+    // peers may still be storing into our exported buffers (replica rows,
+    // gradient receive slots): a rendezvous before anything is freed
+    try {
+      barrier_on_comm();
+    } catch (const tsd::Failure&) {
+    }
+  }
   if (comm) cudaStreamSynchronize(comm);
+  if (grp && attached) {
+    try {
+      if (ready) tsd::group_wait(grp);  // every rank is past its last rendezvous
+    } catch (const tsd::Failure&) {
+    }
+    tsd::group_detach(grp, g);
+    attached = false;
+  }
   if (world) ncclCommDestroy(world);
   if (intra) ncclCommDestroy(intra);
   if (cross) ncclCommDestroy(cross);
@@ -1336,7 +1528,7 @@ void ts_table::destroy() {
                   &entry_vals, &bucket, &order, &send_ids, &recv_ids, &bucket_start, &all_counts}) {
     b->release();
   }
-  for (auto* b : {&partials, &send_rows, &recv_rows, &dense_dp, &dense_flex}) b->release();
+  for (auto* b : {&partials, &send_rows, &recv_rows, &dense_dp, &dense_flex, &ar_tmp}) b->release();
   stamp_dp.release();
   stamp_flex.release();
   for (auto& [a, b] : ev_pool) {
@@ -1376,6 +1568,7 @@ ts_status ts_table_create(ts_table** out, const ts_table_config* cfg, const uint
     auto t = std::make_unique<ts_table>();
     try {
       t->create(*cfg, tier_dest);
+      t->ready = true;
     } catch (...) {
       t->destroy();
       throw;
@@ -1535,23 +1728,19 @@ ts_status ts_table_counters(ts_table* t, uint64_t* counters) {
     std::memset(counters, 0, sizeof(uint64_t) * TS_NUM_COUNTERS * U);
     unsigned long long tiers[3] = {0, 0, 0};
     uint32_t nseg = 0;
+    if (U == 1 && t->last_occ) {
+      // tiers are not bucketed at U == 1 (every occurrence is local): count
+      // them from the placement cuts over the last batch, on the device
+      const unsigned grid = static_cast<unsigned>(
+          std::min<uint64_t>((t->last_occ + 255) / 256, 4u * tsd::sm_count()));
+      TSD_CUDA(cudaMemsetAsync(t->tier_counts.ptr, 0, sizeof(unsigned long long) * 3, t->stream));
+      tsd::count_tiers_kernel<<<grid, 256, 0, t->stream>>>(t->last_rows, t->last_occ, t->cfg.dp_cut,
+                                                      t->cfg.flex_cut, t->tier_counts.ptr);
+      TSD_LAUNCH_CHECK();
+    }
     TSD_CUDA(cudaMemcpyAsync(tiers, t->tier_counts.ptr, sizeof(tiers), cudaMemcpyDeviceToHost, t->stream));
     TSD_CUDA(cudaMemcpyAsync(&nseg, t->nseg.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, t->stream));
     TSD_CUDA(cudaStreamSynchronize(t->stream));
-    if (U == 1) {
-      // tiers are not bucketed at U == 1; count them from the placement cuts
-      // on the device-less path: every occurrence is local.
-      std::vector<uint32_t> rows(t->last_occ);
-      if (t->last_occ) {
-        TSD_CUDA(cudaMemcpy(rows.data(), t->last_rows, sizeof(uint32_t) * t->last_occ,
-                            cudaMemcpyDeviceToHost));
-      }
-      for (const uint32_t c : rows) {
-        if (c < t->cfg.dp_cut) ++tiers[2];
-        else if (c < t->cfg.flex_cut) ++tiers[1];
-        else ++tiers[0];
-      }
-    }
     // requester column g
     counters[TS_CTR_RECV_GLOBAL * U + g] = tiers[0];
     counters[TS_CTR_RECV_INTRA * U + g] = tiers[1];
@@ -1589,25 +1778,48 @@ ts_status ts_table_counters(ts_table* t, uint64_t* counters) {
 ts_status ts_table_read_rows(ts_table* t, const uint32_t* rows, uint64_t count, float* h_weights,
                              float* h_state) {
   return tsd::guarded([&] {
+    using namespace tsd;
     if (!t || (count && (!rows || !h_weights))) tsd::fail(TS_ERR_CONFIG, "ts_table_read_rows: null argument");
     TSD_CUDA(cudaSetDevice(t->cfg.device));
-    TSD_CUDA(cudaStreamSynchronize(t->stream));
     const uint32_t dim = t->cfg.dim;
+    // local ids resolved on the host (all rejected before any copy), then per
+    // chunk: one upload, a row gather (+ state gather) into staging, one D2H
+    std::vector<uint32_t> lids(count);
     for (uint64_t k = 0; k < count; ++k) {
       const uint32_t c = rows[k];
       if (c >= t->cfg.n_rows) tsd::fail(TS_ERR_VALIDATION, "read_rows: row outside the plan");
-      uint64_t lid = c;
+      uint32_t lid = c;
       if (t->U > 1 && c >= t->cfg.dp_cut) {
         const uint8_t d = t->h_dest[c];
         const bool mine = c < t->cfg.flex_cut ? d == t->slot : d == t->g;
         if (!mine) tsd::fail(TS_ERR_VALIDATION, "read_rows: row is not stored on this rank");
         lid = t->h_local[c];
       }
-      TSD_CUDA(cudaMemcpy(h_weights + k * dim, t->d_w + lid * dim, sizeof(float) * dim,
-                          cudaMemcpyDeviceToHost));
-      if (h_state && t->d_state) {
-        TSD_CUDA(cudaMemcpy(h_state + k, t->d_state + lid, sizeof(float), cudaMemcpyDeviceToHost));
+      lids[k] = lid;
+    }
+    if (count == 0) return;
+    TSD_CUDA(cudaStreamSynchronize(t->stream));
+    const uint64_t chunk = std::min<uint64_t>(count, std::max<uint64_t>(1, (uint64_t{64} << 20) / dim));
+    DevBuf<uint32_t> d_ids;
+    DevBuf<float> d_rows, d_st;
+    d_ids.ensure(chunk);
+    d_rows.ensure(chunk * dim);
+    const bool with_state = h_state && t->d_state;
+    if (with_state) d_st.ensure(chunk);
+    for (uint64_t k0 = 0; k0 < count; k0 += chunk) {
+      const uint64_t m = std::min(chunk, count - k0);
+      TSD_CUDA(cudaMemcpyAsync(d_ids.ptr, lids.data() + k0, sizeof(uint32_t) * m, cudaMemcpyHostToDevice,
+                               t->stream));
+      launch_copy_rows(t->d_w, d_ids.ptr, d_rows.ptr, nullptr, m, dim, t->stream);
+      TSD_CUDA(cudaMemcpyAsync(h_weights + k0 * dim, d_rows.ptr, sizeof(float) * m * dim, cudaMemcpyDeviceToHost,
+                               t->stream));
+      if (with_state) {
+        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((m + 255) / 256, 4u * sm_count()));
+        tsd::gather_scalars_kernel<<<grid, 256, 0, t->stream>>>(t->d_state, d_ids.ptr, d_st.ptr, m);
+        TSD_LAUNCH_CHECK();
+        TSD_CUDA(cudaMemcpyAsync(h_state + k0, d_st.ptr, sizeof(float) * m, cudaMemcpyDeviceToHost, t->stream));
       }
+      TSD_CUDA(cudaStreamSynchronize(t->stream));  // staging reused by the next chunk
     }
   });
 }
@@ -1616,6 +1828,17 @@ ts_status ts_table_synchronize(ts_table* t) {
   return tsd::guarded([&] {
     if (!t) tsd::fail(TS_ERR_CONFIG, "ts_table_synchronize: null table");
     TSD_CUDA(cudaSetDevice(t->cfg.device));
+    if (t->p2p) {
+      // collective: peers store into our replicated rows and receive
+      // buffers, so "our step is done" means every rank's step is done --
+      // a rendezvous behind all of this rank's streams, then wait for it
+      for (cudaStream_t s : {t->stream, t->aux}) {
+        if (!s) continue;
+        TSD_CUDA(cudaEventRecord(t->ev_ar, s));
+        TSD_CUDA(cudaStreamWaitEvent(t->comm, t->ev_ar, 0));
+      }
+      t->barrier_on_comm();
+    }
     TSD_CUDA(cudaStreamSynchronize(t->stream));
     if (t->aux) TSD_CUDA(cudaStreamSynchronize(t->aux));
     if (t->comm) TSD_CUDA(cudaStreamSynchronize(t->comm));

@@ -154,7 +154,10 @@ Json traffic_json(const ts::IterationBatch& b, const ts::RowDistribution& d,
   const double row_bytes = static_cast<double>(cfg.embedding_dim) * cfg.scalar_bytes;
   uint64_t plan_global = 0, plan_intra = 0, plan_global_off = 0, plan_intra_off = 0;
   uint64_t rw_off = 0, tw_off = 0, total = 0;
+  // per-server sends, self-inclusive (the reference's convention) and
+  // off-device only: the most loaded server is the all-to-all's critical path
   std::vector<uint64_t> rw_send(u, 0), tw_send(u, 0), plan_send(u, 0);
+  std::vector<uint64_t> rw_send_off(u, 0), tw_send_off(u, 0), plan_send_off(u, 0);
   for (uint32_t g = 0; g < u; ++g) {
     const uint64_t lo = b.sample_offsets[uint64_t{g} * b.local_batch];
     const uint64_t hi = b.sample_offsets[uint64_t{g + 1} * b.local_batch];
@@ -169,14 +172,20 @@ Json traffic_json(const ts::IterationBatch& b, const ts::RowDistribution& d,
       tw_off += tw_owner != g;
       ++rw_send[rw_owner];
       ++tw_send[tw_owner];
+      rw_send_off[rw_owner] += rw_owner != g;
+      tw_send_off[tw_owner] += tw_owner != g;
       const ts::RowPlacement& p = pl[r];
       if (p.tier == ts::Tier::kRowWise) {
         ++plan_global;
         plan_global_off += p.owner_gpu != g;
         ++plan_send[p.owner_gpu];
+        plan_send_off[p.owner_gpu] += p.owner_gpu != g;
       } else if (p.tier == ts::Tier::kFlex) {
+        const uint32_t server = node_base + p.flex_slot;
         ++plan_intra;
-        plan_intra_off += node_base + p.flex_slot != g;
+        plan_intra_off += server != g;
+        ++plan_send[server];
+        plan_send_off[server] += server != g;
       }
     }
   }
@@ -186,8 +195,7 @@ Json traffic_json(const ts::IterationBatch& b, const ts::RowDistribution& d,
               {"reference_convention",
                {{"plan_global_bytes", plan_global * row_bytes},
                 {"plan_intra_bytes", plan_intra * row_bytes},
-                {"rw_global_bytes", total * row_bytes},
-                {"tw_global_bytes", total * row_bytes}}},
+                {"rw_global_bytes", total * row_bytes}}},
               {"off_device",
                {{"plan_global_bytes", plan_global_off * row_bytes},
                 {"plan_intra_bytes", plan_intra_off * row_bytes},
@@ -196,7 +204,11 @@ Json traffic_json(const ts::IterationBatch& b, const ts::RowDistribution& d,
               {"max_send_bytes",
                {{"plan", maxv(plan_send) * row_bytes},
                 {"rw", maxv(rw_send) * row_bytes},
-                {"tw", maxv(tw_send) * row_bytes}}}};
+                {"tw", maxv(tw_send) * row_bytes}}},
+              {"max_send_off_device_bytes",
+               {{"plan", maxv(plan_send_off) * row_bytes},
+                {"rw", maxv(rw_send_off) * row_bytes},
+                {"tw", maxv(tw_send_off) * row_bytes}}}};
 }
 
 Json run(const Json& spec) {

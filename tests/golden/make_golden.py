@@ -12,6 +12,8 @@ Outputs
   mini_2x4_3tier.npz   placements, 4 iterations of batches and the per-GPU
                        counter block of each iteration (restated counters,
                        verified here against the reference's SimReport)
+  c2_full_*.ref.json   (--c2) full-C2 simulate() documents (tests/specs.py
+                       C2_SIM_SPECS)
   io_digests.json      (--io) sha256 of every artefact oracle/_ref/ref_artifacts
                        writes for tests/test_io_parity.py's manifests, and
                        the reference's error text for each malformed one
@@ -28,7 +30,16 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 sys.path.insert(0, str(HERE.parent))
 import oracle_bind as orc  # noqa: E402
-from specs import PLAN_SPECS, REF_DRIVER, SIM_SPECS, run_driver, strip  # noqa: E402
+from specs import C2_SIM_SPECS, PLAN_SPECS, REF_DRIVER, SIM_SPECS, run_driver, strip  # noqa: E402
+
+
+def make_c2() -> None:
+    """Full-C2 simulate() documents (long: ~1-2 min of reference time each)."""
+    with tempfile.TemporaryDirectory() as td:
+        for name, spec in C2_SIM_SPECS.items():
+            doc = strip(run_driver(REF_DRIVER, spec, Path(td), name))
+            (HERE / f"{name}.ref.json").write_text(json.dumps(doc) + "\n")
+            print("wrote", name)
 
 
 def main() -> None:
@@ -111,5 +122,7 @@ def make_io_digests() -> None:
 if __name__ == "__main__":
     if "--io" in sys.argv:
         make_io_digests()
+    elif "--c2" in sys.argv:
+        make_c2()
     else:
         main()

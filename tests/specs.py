@@ -75,6 +75,18 @@ SIM_SPECS = {
                            goal="3tier", workload=dict(seed=9, iterations=2), baseline=True, threads=2),
 }
 
+# Full C2 (BASELINE configs[1]: 8 tables x 10M rows, D=128, L=128/table,
+# B=4096/GPU) at logical U=8, one sampled iteration: the routing loop at the
+# scale the bench runs (33.6M occurrences).  ~1-2 min per reference run.
+C2_SIM_SPECS = {
+    "c2_full_1x8_2tier": dict(tables=tables(8, 10_000_000, 1.05, 128), topology=topo(1, 8),
+                              cost_model=dict(local_batch=4096, embedding_dim=128), goal="2tier",
+                              workload=dict(seed=7, iterations=1), threads=8),
+    "c2_full_2x4_3tier": dict(tables=tables(8, 10_000_000, 1.05, 128), topology=topo(2, 4, PAPER_BW),
+                              cost_model=dict(local_batch=4096, embedding_dim=128), goal="3tier",
+                              workload=dict(seed=7, iterations=1), threads=8),
+}
+
 
 def run_driver(driver: Path, spec: dict, workdir: Path, name: str) -> dict:
     spec_path = workdir / f"{name}.spec.json"

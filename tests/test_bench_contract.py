@@ -38,6 +38,16 @@ def test_reference_arm_contract(tmp_path):
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
     assert d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    # like for like: routing + accounting only (the pool's sampling time is
+    # subtracted), and the exact config dict our arm prints for this workload
+    t = d["reference_timing"]
+    assert 0 < t["materialize_parallel_s"] < t["simulate_s"]
+    assert d["value_including_sampling"] < d["value"]
+    sys.path.insert(0, str(ROOT))
+    import bench
+    ns = bench.parse_args(SMALL)
+    c = d["config"]
+    assert c == bench.job_config(ns, 1, 1, c["plan"], c["dp_cut"], c["flex_cut"])
 
 
 def test_our_arm_has_no_cpu_fallback(tmp_path):

@@ -32,7 +32,7 @@ def test_library_exports_every_symbol():
     lib = ts.load()
     for s in declared_symbols():
         assert hasattr(lib, s)
-    assert lib.ts_abi_version() == 1
+    assert lib.ts_abi_version() == 2
     assert "sm_100a" in ts.build_info()
 
 
@@ -46,6 +46,18 @@ def test_no_cpu_fallback_without_device():
         ts.Router(10, 0, 0, np.zeros(10, np.uint8), 1, 1)
     assert e.value.kind == "NoDevice"
     assert "no CPU fallback" in e.value.message
+
+
+def test_group_host_side():
+    """ts_group is host-only until a table attaches: create / destroy work
+    without a device, bad sizes are ConfigErrors."""
+    g = ts.Group(4)
+    assert g.ranks == 4 and g.handle
+    g.close()
+    for bad in (0, 257):
+        with pytest.raises(ts.TSError) as e:
+            ts.Group(bad)
+        assert e.value.kind == "ConfigError"
 
 
 def test_config_errors_before_device():

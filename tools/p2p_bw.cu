@@ -7,10 +7,15 @@
 //                  (r % (G-1)) -- the serve / gradient-push pattern, all-to-all
 //   local_rows   : random local read + local write (reference)
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a tools/p2p_bw.cu -o tools/p2p_bw
+//   (__graft_entry__.build() does this).
+// Usage: p2p_bw [G] [--json]: --json measures only the exchange patterns
+// (gather_store, store_rows) and prints one JSON line with the best grid's
+// GB/s per GPU per direction -- the NVLink ceiling bench.py reports against.
 #include <cstdint>
 #include <cstdio>
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 #include <vector>
 #include <cuda_runtime.h>
 
@@ -67,8 +72,11 @@ int main(int argc, char** argv) {
     CK(cudaMemset(buf[g], 0, (size_t)slots * 512));
     CK(cudaStreamCreate(&st[g]));
   }
+  const bool json = argc > 2 && std::string(argv[2]) == "--json";
   const char* names[] = {"store_rows", "load_rows", "gather_store", "local_rows"};
+  float best[4] = {0, 0, 0, 0};
   for (int mode = 0; mode < 4; ++mode) {
+    if (json && mode != 0 && mode != 2) continue;
     for (int bps : {1, 2, 4, 8}) {
       for (int infl : {4, 8}) {
         std::vector<cudaEvent_t> e0(G), e1(G);
@@ -90,9 +98,17 @@ int main(int argc, char** argv) {
           worst = 0;
           for (int g = 0; g < G; ++g) { CK(cudaSetDevice(g)); CK(cudaEventSynchronize(e1[g])); float ms; CK(cudaEventElapsedTime(&ms, e0[g], e1[g])); worst = std::max(worst, ms); }
         }
-        printf("G=%d %-12s blocks/SM=%d inflight=%d: %.3f ms  %.1f GB/s per GPU (one direction)\n", G, names[mode], bps, infl, worst, rows * 512.0 / worst / 1e6);
+        const float gbs = rows * 512.0 / worst / 1e6;
+        best[mode] = std::max(best[mode], gbs);
+        for (int g = 0; g < G; ++g) { CK(cudaEventDestroy(e0[g])); CK(cudaEventDestroy(e1[g])); }
+        if (!json) printf("G=%d %-12s blocks/SM=%d inflight=%d: %.3f ms  %.1f GB/s per GPU (one direction)\n", G, names[mode], bps, infl, worst, gbs);
       }
     }
+  }
+  if (json) {
+    printf("{\"gpus\": %d, \"gather_store_gbs\": %.1f, \"store_rows_gbs\": %.1f, \"rows_bytes\": 512, "
+           "\"what\": \"best over grids of 1-8 blocks/SM, every GPU at once, per GPU per direction\"}\n",
+           G, best[2], best[0]);
   }
   return 0;
 }
