@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <memory>
 #include <vector>
 
@@ -67,21 +69,20 @@ __device__ __forceinline__ void classify(const RouteParams& p, uint32_t r, uint3
   }
 }
 
-// First touch of (server, r) this iteration (the reference's stamps,
-// simulator.cpp:158-166,250-255): test, then claim with an atomic OR.
-__device__ __forceinline__ bool first_touch(const RouteParams& p, uint32_t r, uint32_t kind, uint32_t g) {
-  uint64_t bit;
-  if (kind == 0) {
-    bit = r - p.flex_cut;
-  } else if (kind == 1) {
-    bit = p.flex_base + static_cast<uint64_t>(g / p.w) * (p.flex_cut - p.dp_cut) + (r - p.dp_cut);
-  } else {
-    bit = p.dp_base + static_cast<uint64_t>(g) * p.dp_cut + r;
-  }
-  uint32_t* word = p.seen + (bit >> 5);
-  const uint32_t m = 1u << (bit & 31);
-  if ((*reinterpret_cast<volatile uint32_t*>(word) & m) != 0) return false;
-  return (atomicOr(word, m) & m) == 0;
+// Bit of (server, r) in the compact distinct bitmap.
+__device__ __forceinline__ uint64_t seen_bit(const RouteParams& p, uint32_t r, uint32_t kind, uint32_t g) {
+  if (kind == 0) return r - p.flex_cut;
+  if (kind == 1) return p.flex_base + static_cast<uint64_t>(g / p.w) * (p.flex_cut - p.dp_cut) + (r - p.dp_cut);
+  return p.dp_base + static_cast<uint64_t>(g) * p.dp_cut + r;
+}
+
+// Marks (server, r) as served this iteration (the reference's stamps,
+// simulator.cpp:158-166): a fire-and-forget atomic OR -- the result is not
+// read, so it compiles to a RED and costs the routing loop no round trip.
+// The distinct counts come from one pass over the bitmap afterwards
+// (distinct_count_kernel).
+__device__ __forceinline__ void mark(const RouteParams& p, uint64_t bit) {
+  atomicOr(p.seen + (bit >> 5), 1u << (bit & 31));
 }
 
 // General U (<= 256): warp-aggregated shared-memory counters.
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(kRouterThreads) route_count_kernel(RouteParams
 
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   // Uniform trip count per warp: every lane runs the same iterations so the
-  // match/ballot intrinsics always see the full warp.
+  // match intrinsics always see the full warp.
   for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x; base < p.occ; base += stride) {
     const uint64_t idx = base + threadIdx.x;
     bool valid = idx < p.occ;
@@ -117,6 +118,9 @@ __global__ void __launch_bounds__(kRouterThreads) route_count_kernel(RouteParams
       }
       g = lo;
       classify(p, r, g, kind, server);
+      // test first: a Zipf-hot row would otherwise pile REDs onto one word
+      const uint64_t bit = seen_bit(p, r, kind, g);
+      if ((*reinterpret_cast<volatile uint32_t*>(p.seen + (bit >> 5)) & (1u << (bit & 31))) == 0) mark(p, bit);
     }
     // requester-side counter: RECV_GLOBAL / RECV_INTRA / DP_LOCAL [g]
     const unsigned req_ctr = kind == 0 ? TS_CTR_RECV_GLOBAL
@@ -127,7 +131,6 @@ __global__ void __launch_bounds__(kRouterThreads) route_count_kernel(RouteParams
     const unsigned send_ctr = kind == 0 ? TS_CTR_SEND_GLOBAL : TS_CTR_SEND_INTRA;
     warp_count(s_cnt, send_ctr * u + server, sends);
     warp_count(s_cnt, TS_CTR_SERVED * u + server, valid);
-    warp_count(s_cnt, TS_CTR_DISTINCT * u + server, valid && first_touch(p, r, kind, g));
   }
   __syncthreads();
   for (unsigned i = threadIdx.x; i < TS_NUM_COUNTERS * u; i += blockDim.x) {
@@ -141,116 +144,220 @@ __device__ __forceinline__ void add_at(uint32_t (&c)[K], uint32_t i, uint32_t v)
   for (int k = 0; k < K; ++k) c[k] += i == static_cast<uint32_t>(k) ? v : 0u;
 }
 
-// U <= 8 (one NVSwitch node): per-thread register counters, no warp
-// intrinsics on the per-occurrence path.  A thread's grid-stride indices
-// ascend, so its requester only moves forward (the per-requester counts
-// are flushed when it does); server-side counts are per-thread arrays of 8
-// updated by predicated adds; SERVED is not counted at all -- it equals
-// SEND_GLOBAL + SEND_INTRA + DP_LOCAL per GPU (a DP row is served by its
-// requester) and the host derives it.  Warp shuffle + shared atomics once
-// per thread at the end.
-__global__ void __launch_bounds__(kRouterThreads) route_count_u8_kernel(RouteParams p) {
+// U <= 8 (one NVSwitch node).  Each block takes a contiguous chunk of ONE
+// requester's occurrences (grid = U x blocks_per_req), so:
+//   * the requester-side counts are three registers per thread;
+//   * a shared-memory bitmap over the hottest canonical rows (r < kFilterRows:
+//     canonical order is probability order, so these carry most of a Zipf
+//     batch) filters the distinct marks -- a hot row reaches the global
+//     bitmap once per block instead of once per occurrence;
+//   * server-side counts are per-thread arrays of 8 updated by predicated
+//     adds; SERVED is not counted at all -- it equals SEND_GLOBAL +
+//     SEND_INTRA + DP_LOCAL per GPU (a DP row is served by its requester)
+//     and the host derives it.
+// No warp intrinsics on the per-occurrence path; warp shuffles + shared
+// atomics once per thread at the end.
+constexpr int kU8Threads = 512;
+constexpr uint32_t kFilterRows = 1u << 19;  // 64 KB of shared memory (dynamic)
+__global__ void __launch_bounds__(kU8Threads, 2) route_count_u8_kernel(RouteParams p, uint32_t blocks_per_req) {
+  extern __shared__ uint32_t s_filter[];  // kFilterRows bits
   __shared__ unsigned long long s_cnt[TS_NUM_COUNTERS * kSmallU];
-  __shared__ uint64_t s_bounds[kSmallU + 1];
-  const uint32_t u = p.u;
+  const uint32_t g = blockIdx.x / blocks_per_req, part = blockIdx.x % blocks_per_req;
+  for (unsigned i = threadIdx.x; i < kFilterRows / 32; i += blockDim.x) s_filter[i] = 0;
   for (unsigned i = threadIdx.x; i < TS_NUM_COUNTERS * kSmallU; i += blockDim.x) s_cnt[i] = 0;
-  for (unsigned i = threadIdx.x; i <= u; i += blockDim.x) s_bounds[i] = p.req_begin[i];
   __syncthreads();
+  const uint64_t lo = p.req_begin[g], hi = p.req_begin[g + 1];
+  const uint64_t chunk = (hi - lo + blocks_per_req - 1) / blocks_per_req;
+  const uint64_t begin = lo + part * chunk, end = min(hi, begin + chunk);
+  const uint32_t node_base = (g / p.w) * p.w;
+  const uint64_t flex_sec = p.flex_base + static_cast<uint64_t>(g / p.w) * (p.flex_cut - p.dp_cut) - p.dp_cut;
+  const uint64_t dp_sec = p.dp_base + static_cast<uint64_t>(g) * p.dp_cut;
 
-  uint32_t send_g[kSmallU] = {}, send_i[kSmallU] = {}, dist[kSmallU] = {};
+  uint32_t send_g[kSmallU] = {}, send_i[kSmallU] = {};
   uint32_t req[3] = {0, 0, 0};
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  uint32_t g = 0;
-  while (g + 1 < u && s_bounds[g + 1] <= idx) ++g;
-  const auto flush_req = [&](uint32_t gg) {
-    if (req[0]) atomicAdd(&s_cnt[TS_CTR_RECV_GLOBAL * kSmallU + gg], static_cast<unsigned long long>(req[0]));
-    if (req[1]) atomicAdd(&s_cnt[TS_CTR_RECV_INTRA * kSmallU + gg], static_cast<unsigned long long>(req[1]));
-    if (req[2]) atomicAdd(&s_cnt[TS_CTR_DP_LOCAL * kSmallU + gg], static_cast<unsigned long long>(req[2]));
-    req[0] = req[1] = req[2] = 0;
+  bool bad = false;
+  // one occurrence whose placement byte d is loaded (or unused for DP)
+  const auto route_one = [&](uint32_t r, uint32_t d) {
+    if (r >= p.n_rows) {
+      bad = true;
+      return;
+    }
+    uint64_t bit;
+    if (r < p.dp_cut) {
+      req[2] += 1;
+      bit = dp_sec + r;
+    } else if (r < p.flex_cut) {
+      req[1] += 1;
+      add_at(send_i, node_base + d, 1u);
+      bit = flex_sec + r;
+    } else {
+      req[0] += 1;
+      add_at(send_g, d, 1u);
+      bit = r - p.flex_cut;
+    }
+    bool first = true;
+    if (r < kFilterRows) {
+      const uint32_t m = 1u << (r & 31);
+      first = (atomicOr(&s_filter[r >> 5], m) & m) == 0;
+    }
+    if (first) mark(p, bit);
   };
-  // kBatch independent occurrences per thread per trip (indices idx,
-  // idx + stride, ...: still ascending): their index, placement-byte and
-  // bitmap loads are issued together, so each thread keeps kBatch dependent
-  // load chains in flight instead of one
-  constexpr int kBatch = 4;
-  for (; idx < p.occ; idx += kBatch * stride) {
-    uint32_t r[kBatch];
-    bool ok[kBatch];
+  const auto dest_of = [&](uint32_t r) -> uint32_t {
+    return r >= p.dp_cut && r < p.n_rows ? __ldg(p.dest + r) : 0u;
+  };
+  // body: 16 B-aligned uint4 loads of 4 indices, two per thread per trip,
+  // and the next trip's two issued before this trip's placement bytes --
+  // the index stream stays in flight behind the dependent byte loads
+  const uint64_t a0 = min(end, (begin + 3) & ~uint64_t{3});
+  const uint64_t a1 = max(a0, end & ~uint64_t{3});
+  const uint4* vec = reinterpret_cast<const uint4*>(p.rows + a0);
+  const uint64_t nvec = (a1 - a0) / 4;
+  const uint4 zero4 = make_uint4(0, 0, 0, 0);
+  uint64_t j = threadIdx.x;
+  uint4 va = j < nvec ? __ldg(vec + j) : zero4;
+  uint4 vb = j + kU8Threads < nvec ? __ldg(vec + j + kU8Threads) : zero4;
+  for (; j < nvec; j += 2 * kU8Threads) {
+    const uint64_t jn = j + 2 * kU8Threads;
+    const uint4 na = jn < nvec ? __ldg(vec + jn) : zero4;
+    const uint4 nb = jn + kU8Threads < nvec ? __ldg(vec + jn + kU8Threads) : zero4;
+    const bool has_b = j + kU8Threads < nvec;
+    const uint32_t r[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+    uint32_t d[8];
 #pragma unroll
-    for (int k = 0; k < kBatch; ++k) {
-      const uint64_t i = idx + k * stride;
-      ok[k] = i < p.occ;
-      r[k] = ok[k] ? __ldg(p.rows + i) : 0u;
-      if (ok[k] && r[k] >= p.n_rows) {
-        atomicAdd(p.bad_rows, 1u);
-        ok[k] = false;
-      }
+    for (int k = 0; k < 8; ++k) d[k] = (k < 4 || has_b) ? dest_of(r[k]) : 0u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k < 4 || has_b) route_one(r[k], d[k]);
     }
-    uint32_t d[kBatch];
-#pragma unroll
-    for (int k = 0; k < kBatch; ++k) d[k] = ok[k] && r[k] >= p.dp_cut ? __ldg(p.dest + r[k]) : 0u;
-    uint32_t* word[kBatch];
-    uint32_t mask[kBatch], server[kBatch];
-#pragma unroll
-    for (int k = 0; k < kBatch; ++k) {
-      word[k] = nullptr;
-      mask[k] = 0;
-      server[k] = 0;
-      if (!ok[k]) continue;
-      const uint64_t i = idx + k * stride;
-      if (s_bounds[g + 1] <= i) {
-        flush_req(g);
-        do ++g; while (g + 1 < u && s_bounds[g + 1] <= i);
-      }
-      uint64_t bit;
-      if (r[k] < p.dp_cut) {
-        req[2] += 1;
-        server[k] = g;
-        bit = p.dp_base + static_cast<uint64_t>(g) * p.dp_cut + r[k];
-      } else if (r[k] < p.flex_cut) {
-        req[1] += 1;
-        server[k] = (g / p.w) * p.w + d[k];
-        add_at(send_i, server[k], 1u);
-        bit = p.flex_base + static_cast<uint64_t>(g / p.w) * (p.flex_cut - p.dp_cut) + (r[k] - p.dp_cut);
-      } else {
-        req[0] += 1;
-        server[k] = d[k];
-        add_at(send_g, server[k], 1u);
-        bit = r[k] - p.flex_cut;
-      }
-      word[k] = p.seen + (bit >> 5);
-      mask[k] = 1u << (bit & 31);
-    }
-    uint32_t cur[kBatch];
-#pragma unroll
-    for (int k = 0; k < kBatch; ++k) cur[k] = word[k] ? *reinterpret_cast<volatile uint32_t*>(word[k]) : ~0u;
-#pragma unroll
-    for (int k = 0; k < kBatch; ++k) {
-      if ((cur[k] & mask[k]) == 0 && (atomicOr(word[k], mask[k]) & mask[k]) == 0) add_at(dist, server[k], 1u);
-    }
+    va = na;
+    vb = nb;
   }
-  flush_req(g);
+  // unaligned head [begin, a0) and tail [a1, end): at most 3 + 3 indices
+  if (threadIdx.x < a0 - begin) {
+    const uint32_t r = __ldg(p.rows + begin + threadIdx.x);
+    route_one(r, dest_of(r));
+  }
+  if (threadIdx.x < end - a1) {
+    const uint32_t r = __ldg(p.rows + a1 + threadIdx.x);
+    route_one(r, dest_of(r));
+  }
+  if (bad) atomicAdd(p.bad_rows, 1u);
+  atomicAdd(&s_cnt[TS_CTR_RECV_GLOBAL * kSmallU + g], static_cast<unsigned long long>(req[0]));
+  atomicAdd(&s_cnt[TS_CTR_RECV_INTRA * kSmallU + g], static_cast<unsigned long long>(req[1]));
+  atomicAdd(&s_cnt[TS_CTR_DP_LOCAL * kSmallU + g], static_cast<unsigned long long>(req[2]));
   const unsigned lane = threadIdx.x & 31u;
 #pragma unroll
   for (int s = 0; s < kSmallU; ++s) {
-    uint32_t a = send_g[s], b = send_i[s], c = dist[s];
+    uint32_t a = send_g[s], b = send_i[s];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
       b += __shfl_xor_sync(0xFFFFFFFFu, b, o);
-      c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
     }
     if (lane == 0) {
       if (a) atomicAdd(&s_cnt[TS_CTR_SEND_GLOBAL * kSmallU + s], static_cast<unsigned long long>(a));
       if (b) atomicAdd(&s_cnt[TS_CTR_SEND_INTRA * kSmallU + s], static_cast<unsigned long long>(b));
-      if (c) atomicAdd(&s_cnt[TS_CTR_DISTINCT * kSmallU + s], static_cast<unsigned long long>(c));
     }
   }
   __syncthreads();
   for (unsigned i = threadIdx.x; i < TS_NUM_COUNTERS * kSmallU; i += blockDim.x) {
     const unsigned ctr = i / kSmallU, gpu = i % kSmallU;
-    if (gpu < u && s_cnt[i]) atomicAdd(p.counters + ctr * u + gpu, s_cnt[i]);
+    if (gpu < p.u && s_cnt[i]) atomicAdd(p.counters + ctr * p.u + gpu, s_cnt[i]);
+  }
+}
+
+// Distinct counts for U <= 8 (see distinct_count_kernel below): one thread
+// per bitmap word, per-thread register counters, one reduction at the end.
+__global__ void __launch_bounds__(256) distinct_count_u8_kernel(RouteParams p, uint64_t words) {
+  __shared__ unsigned long long s_cnt[kSmallU];
+  if (threadIdx.x < kSmallU) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  uint32_t cnt[kSmallU] = {};
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t flex_rows = p.flex_cut - p.dp_cut;
+  const uint64_t total_bits = p.dp_base + static_cast<uint64_t>(p.u) * p.dp_cut;
+  for (uint64_t wi = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; wi < words; wi += stride) {
+    uint32_t m = p.seen[wi];
+    const uint64_t b0 = wi * 32;
+    if (b0 + 32 > total_bits) m &= b0 >= total_bits ? 0u : (1u << (total_bits - b0)) - 1u;
+    while (m) {
+      const uint64_t bit = b0 + (__ffs(m) - 1);
+      if (bit >= p.dp_base) {  // DP: every set bit up to the section end is one requester's
+        const uint64_t g = (bit - p.dp_base) / p.dp_cut;
+        const uint64_t end = p.dp_base + (g + 1) * p.dp_cut;
+        uint32_t same = m;
+        if (end < b0 + 32) same &= (1u << (end - b0)) - 1u;
+        add_at(cnt, static_cast<uint32_t>(g), __popc(same));
+        m &= ~same;
+        continue;
+      }
+      uint32_t server;
+      if (bit >= p.flex_base) {
+        const uint64_t rel = bit - p.flex_base;
+        server = static_cast<uint32_t>((rel / flex_rows) * p.w) + __ldg(p.dest + p.dp_cut + rel % flex_rows);
+      } else {
+        server = __ldg(p.dest + p.flex_cut + bit);
+      }
+      add_at(cnt, server, 1u);
+      m &= m - 1;
+    }
+  }
+  const unsigned lane = threadIdx.x & 31u;
+#pragma unroll
+  for (int s = 0; s < kSmallU; ++s) {
+    uint32_t a = cnt[s];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
+    if (lane == 0 && a) atomicAdd(&s_cnt[s], static_cast<unsigned long long>(a));
+  }
+  __syncthreads();
+  if (threadIdx.x < p.u && s_cnt[threadIdx.x]) {
+    atomicAdd(p.counters + TS_CTR_DISTINCT * p.u + threadIdx.x, s_cnt[threadIdx.x]);
+  }
+}
+
+// Distinct (server, row) pairs per server from the marked bitmap: the RW
+// section is one bit per RW row (server = its owner byte), the Flex section
+// one bit per (node, Flex row) (server = node*W + slot byte), the DP section
+// one bit per (requester, DP row) (server = requester).  One thread per
+// 32-bit word: popcount when the word has one server, else per set bit.
+__global__ void __launch_bounds__(256) distinct_count_kernel(RouteParams p, uint64_t words) {
+  __shared__ unsigned s_cnt[kMaxGpus];
+  for (unsigned i = threadIdx.x; i < p.u; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t flex_rows = p.flex_cut - p.dp_cut;
+  const uint64_t total_bits = p.dp_base + static_cast<uint64_t>(p.u) * p.dp_cut;
+  for (uint64_t wi = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; wi < words; wi += stride) {
+    uint32_t m = p.seen[wi];
+    while (m) {
+      const int b = __ffs(m) - 1;
+      const uint64_t bit = wi * 32 + b;
+      if (bit >= total_bits) break;
+      if (bit >= p.dp_base) {  // DP: the rest of the word up to the section end is one requester
+        const uint64_t g = (bit - p.dp_base) / p.dp_cut;
+        const uint64_t end = p.dp_base + (g + 1) * p.dp_cut;  // first bit of the next requester
+        uint32_t same = m;
+        if (end < wi * 32 + 32) same &= (1u << (end - wi * 32)) - 1u;
+        atomicAdd(&s_cnt[g], __popc(same));
+        m &= ~same;
+        continue;
+      }
+      uint32_t server;
+      if (bit >= p.flex_base) {
+        const uint64_t rel = bit - p.flex_base;
+        const uint64_t node = rel / flex_rows;
+        server = static_cast<uint32_t>(node * p.w) + p.dest[p.dp_cut + rel % flex_rows];
+      } else {
+        server = p.dest[p.flex_cut + bit];
+      }
+      atomicAdd(&s_cnt[server], 1u);
+      m &= m - 1;
+    }
+  }
+  __syncthreads();
+  for (unsigned i = threadIdx.x; i < p.u; i += blockDim.x) {
+    if (s_cnt[i]) atomicAdd(p.counters + TS_CTR_DISTINCT * p.u + i, static_cast<unsigned long long>(s_cnt[i]));
   }
 }
 
@@ -284,21 +391,44 @@ struct ts_router {
     TSD_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned), stream));
     TSD_CUDA(cudaMemsetAsync(d_seen, 0, sizeof(uint32_t) * seen_words, stream));
     TSD_CUDA(cudaEventRecord(ev[1], stream));
-    const bool small = U <= kSmallU;
+    // TIERSHARD_ROUTER=general forces the warp-aggregated kernel (A/B)
+    static const bool force_general = [] {
+      const char* e = std::getenv("TIERSHARD_ROUTER");
+      return e && std::string(e) == "general";
+    }();
+    const bool small = U <= kSmallU && !force_general;
     if (occ > 0) {
       RouteParams p{rows, occ, d_req_begin, d_dest, n_rows, dp_cut, flex_cut, U, gpus_per_node,
                     d_seen, flex_base, dp_base, d_counters, d_bad};
       const unsigned blocks = static_cast<unsigned>(
           std::min<uint64_t>(ceil_div(occ, kRouterThreads), static_cast<uint64_t>(sm_count()) * 4));
       if (small) {
-        // persistent: every resident block once (the grid-stride loop covers the rest)
+        // U x blocks_per_req blocks, each a contiguous chunk of one requester
+        constexpr size_t kFilterBytes = kFilterRows / 8;
+        static const bool attr_set = [] {
+          TSD_CUDA(cudaFuncSetAttribute(route_count_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kFilterBytes)));
+          return true;
+        }();
+        (void)attr_set;
         int per_sm = 0;
-        TSD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, route_count_u8_kernel, kRouterThreads, 0));
-        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(
-            ceil_div(occ, kRouterThreads), static_cast<uint64_t>(sm_count()) * std::max(per_sm, 1)));
-        route_count_u8_kernel<<<grid, kRouterThreads, 0, stream>>>(p);
+        TSD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, route_count_u8_kernel, kU8Threads,
+                                                               kFilterBytes));
+        const uint32_t bpr = static_cast<uint32_t>(std::max<uint64_t>(
+            1, std::min<uint64_t>(ceil_div(occ, uint64_t{U} * kU8Threads * 16),
+                                  ceil_div(static_cast<uint64_t>(sm_count()) * std::max(per_sm, 1), U))));
+        const unsigned grid = U * bpr;
+        route_count_u8_kernel<<<grid, kU8Threads, kFilterBytes, stream>>>(p, bpr);
       } else {
         route_count_kernel<<<blocks, kRouterThreads, 0, stream>>>(p);
+      }
+      TSD_LAUNCH_CHECK();
+      const unsigned dgrid = static_cast<unsigned>(
+          std::min<uint64_t>(ceil_div(seen_words, 256), static_cast<uint64_t>(sm_count()) * 8));
+      if (small) {
+        distinct_count_u8_kernel<<<dgrid, 256, 0, stream>>>(p, seen_words);
+      } else {
+        distinct_count_kernel<<<dgrid, 256, 0, stream>>>(p, seen_words);
       }
       TSD_LAUNCH_CHECK();
     }
