@@ -398,10 +398,17 @@ def run_ours(args, dist: Dist):
     if u > 1:
         nccl_id = dist.bcast(ts.nccl_unique_id() if g == 0 else None)
     opt = ts.OPT_ROWWISE_ADAGRAD if args.optimizer == "adagrad" else ts.OPT_SGD
+    # gradient receive buffer from the plan: the most loaded server's
+    # off-device requests over the prepared iterations, +25 % (+50 % with
+    # GPU-sampled batches); a step that needs more grows it collectively
+    recv_hint = 0
+    if u > 1:
+        most = max(t["max_send_off_device_bytes"]["plan"] for t in exp["traffic"]) / (D * 4)
+        recv_hint = int(most * (1.5 if sampler is not None else 1.25)) + 4096
     table = ts.Table(n_rows=exp["n_rows"], dim=D, dp_cut=plan["dp_cut"], flex_cut=plan["flex_cut"],
                      tier_dest=dest if u > 1 else None, num_nodes=u // w, gpus_per_node=w, rank=g,
                      device=device, weight_seed=1234, optimizer=opt, lr=args.lr,
-                     max_occurrences=max_occ, nccl_unique_id=nccl_id)
+                     max_occurrences=max_occ, nccl_unique_id=nccl_id, recv_rows_hint=recv_hint)
     stream = torch.cuda.ExternalStream(table.stream(), device=device)
     d_rows = [torch.from_numpy(b.view(np.int32)).to(f"cuda:{device}") for b in batches]
     d_out = torch.empty((max_occ, D), dtype=torch.float32, device=f"cuda:{device}")
@@ -907,8 +914,10 @@ def run_reference(args, dist: Dist):
 
 def main():
     args = parse_args()
-    # stdout carries exactly one JSON line: keep NCCL's banner off it
-    os.environ.setdefault("NCCL_DEBUG", "WARN")
+    # stdout carries exactly one JSON line: with NCCL_DEBUG set (even WARN)
+    # NCCL prints its version banner there, so it stays unset here
+    if not os.environ.get("TS_BENCH_KEEP_NCCL_DEBUG"):
+        os.environ.pop("NCCL_DEBUG", None)
     dist = Dist()
     try:
         if args.impl == "reference":

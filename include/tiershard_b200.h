@@ -267,12 +267,42 @@ typedef struct ts_table_config {
   const void* nccl_unique_id;    /* 128-byte ncclUniqueId (one process per rank) */
   struct ts_group* group;        /* in-process rank group (ts_group_create), or NULL;
                                     U > 1 needs exactly one of nccl_unique_id / group */
+  uint64_t recv_rows_hint;       /* U > 1: initial capacity (rows) of the buffer peers
+                                    push this rank's remote gradients into -- e.g. the
+                                    plan's expected remote occurrences plus a margin;
+                                    0 = the worst case, (U-1) x max_occurrences.  A step
+                                    that needs more grows it (collectively, with 25 %
+                                    headroom) instead of failing. */
 } ts_table_config;
+
+/* Device bytes one rank allocates, itemised (ts_table_plan_footprint). */
+typedef struct ts_table_footprint {
+  uint64_t weights;          /* [local_rows x dim] fp32 shard */
+  uint64_t optimizer_state;  /* row-wise Adagrad state */
+  uint64_t remap;            /* U > 1: placement byte + local id per canonical row */
+  uint64_t step_buffers;     /* dedup sort, segments, piece partials */
+  uint64_t exchange;         /* U > 1: request lists, gradient receive buffer */
+  uint64_t replicated;       /* U > 1: replicated-row receive slots + stamps */
+  uint64_t host_api;         /* ts_table_train_step(s)_host staging + output */
+  uint64_t total;
+} ts_table_footprint;
+
+/* Host-only: what ts_table_create (and, with host_api, the host-buffer
+ * entry points) will allocate on a rank whose shard holds dp_rows /
+ * flex_rows / rw_rows rows (ts_shard_layout's counts).  ts_table_create
+ * checks the same sum against the device's free memory and fails with
+ * TS_ERR_CONFIG before allocating when it does not fit. */
+ts_status ts_table_plan_footprint(const ts_table_config* cfg, uint64_t dp_rows, uint64_t flex_rows,
+                                  uint64_t rw_rows, int host_api, ts_table_footprint* out);
 
 /* Collective over all U ranks when U > 1 (NCCL communicator creation). */
 ts_status ts_table_create(ts_table** out, const ts_table_config* cfg,
                           const uint8_t* tier_dest);
 ts_status ts_table_destroy(ts_table* t);
+
+/* U > 1: current gradient receive-buffer capacity (rows) and how many times
+ * a step has grown it (the bounded-buffer overflow path). */
+ts_status ts_table_recv_capacity(ts_table* t, uint64_t* rows, uint64_t* regrows);
 
 /* Rows of this rank's shard by tier. */
 ts_status ts_table_shard_rows(ts_table* t, uint64_t* dp_rows,

@@ -15,6 +15,7 @@ from .capi import (  # noqa: F401
     Sampler,
     Table,
     Group,
+    plan_footprint,
     load,
     build_info,
     device_count,

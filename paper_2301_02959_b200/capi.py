@@ -80,6 +80,8 @@ EXPORTS = (
     "ts_frontier_preview",
     "ts_group_create",
     "ts_group_destroy",
+    "ts_table_plan_footprint",
+    "ts_table_recv_capacity",
 )
 
 
@@ -108,7 +110,13 @@ class TableConfig(C.Structure):
         ("max_occurrences", C.c_uint64),
         ("nccl_unique_id", C.c_void_p),
         ("group", C.c_void_p),
+        ("recv_rows_hint", C.c_uint64),
     ]
+
+
+class Footprint(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in ("weights", "optimizer_state", "remap", "step_buffers", "exchange",
+                                          "replicated", "host_api", "total")]
 
 
 _lib = None
@@ -175,6 +183,9 @@ def load() -> C.CDLL:
         "ts_frontier_preview": (C.c_int, [C.c_int, C.c_uint64, vp, C.c_uint32, vp, vp]),
         "ts_group_create": (C.c_int, [C.POINTER(vp), C.c_uint32]),
         "ts_group_destroy": (C.c_int, [vp]),
+        "ts_table_recv_capacity": (C.c_int, [vp, u64p, u64p]),
+        "ts_table_plan_footprint": (C.c_int, [C.POINTER(TableConfig), C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
+                                              C.POINTER(Footprint)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -238,6 +249,17 @@ def exchange_plan(num_nodes, gpus_per_node, rank, all_starts):
                                    _ptr(ro), _ptr(rc), C.byref(before), C.byref(total)))
     return dict(send_off=so, send_cnt=sc, recv_off=ro, recv_cnt=rc, recv_before=before.value,
                 recv_total=total.value)
+
+
+def plan_footprint(*, n_rows, dim, dp_rows, flex_rows, rw_rows, num_nodes=1, gpus_per_node=1,
+                   optimizer=OPT_ROWWISE_ADAGRAD, max_occurrences, recv_rows_hint=0, host_api=False) -> dict:
+    """Host-only ts_table_plan_footprint: device bytes one rank allocates."""
+    cfg = TableConfig(num_nodes, gpus_per_node, 0, 0, dim, n_rows, 0, 0, 0, optimizer, 0.0, 0.0,
+                      max_occurrences, None, None, recv_rows_hint)
+    out = Footprint()
+    _check(load().ts_table_plan_footprint(C.byref(cfg), dp_rows, flex_rows, rw_rows, 1 if host_api else 0,
+                                          C.byref(out)))
+    return {k: getattr(out, k) for k, _ in Footprint._fields_}
 
 
 class Router:
@@ -393,12 +415,13 @@ class Table:
                  gpus_per_node: int = 1, rank: int = 0, device: int = 0,
                  weight_seed: int = 1234, optimizer: int = OPT_SGD, lr: float = 0.01,
                  eps: float = 1e-8, max_occurrences: int = 1 << 20,
-                 nccl_unique_id: bytes | None = None, group: Group | None = None):
+                 nccl_unique_id: bytes | None = None, group: Group | None = None,
+                 recv_rows_hint: int = 0):
         self._lib = load()
         self.u = num_nodes * gpus_per_node
         self.dim = dim
         cfg = TableConfig(num_nodes, gpus_per_node, rank, device, dim, n_rows, dp_cut, flex_cut,
-                          weight_seed, optimizer, lr, eps, max_occurrences, None, None)
+                          weight_seed, optimizer, lr, eps, max_occurrences, None, None, recv_rows_hint)
         if group is not None:
             cfg.group = group.handle
             self._group = group  # outlives the table
@@ -457,6 +480,12 @@ class Table:
 
     def synchronize(self) -> None:
         _check(self._lib.ts_table_synchronize(self._h))
+
+    def recv_capacity(self) -> tuple[int, int]:
+        """(receive-buffer rows, times grown) -- U > 1."""
+        a, b = C.c_uint64(), C.c_uint64()
+        _check(self._lib.ts_table_recv_capacity(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def shard_rows(self) -> tuple[int, int, int]:
         a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()

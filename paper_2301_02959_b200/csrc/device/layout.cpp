@@ -3,6 +3,7 @@
 // the per-step all-to-allv plan derived from the all-gathered bucket counts.
 // Pure integer arithmetic; unit-tested on the CPU (tests/test_layout.py,
 // including a gloo world-size-2 exchange-consistency test).
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -102,7 +103,81 @@ ts_status host_guard(F&& f) {
 
 }  // namespace
 
+namespace tsd {
+
+uint64_t recv_capacity_rows(const ts_table_config& c) {
+  const uint64_t U = uint64_t{c.num_nodes} * c.gpus_per_node;
+  const uint64_t worst = (U - 1) * c.max_occurrences;
+  return c.recv_rows_hint ? std::max<uint64_t>(1, std::min(c.recv_rows_hint, worst)) : std::max<uint64_t>(1, worst);
+}
+
+namespace {
+uint64_t paged(uint64_t bytes) {
+  constexpr uint64_t kPage = uint64_t{2} << 20;
+  bytes = std::max<uint64_t>(bytes, 4);
+  return bytes > (kPage >> 1) ? (bytes + kPage - 1) / kPage * kPage : bytes;
+}
+}  // namespace
+
+ts_table_footprint table_footprint(const ts_table_config& c, uint64_t dp_rows, uint64_t flex_rows,
+                                   uint64_t rw_rows, bool host_api) {
+  ts_table_footprint f{};
+  const uint64_t U = uint64_t{c.num_nodes} * c.gpus_per_node;
+  const uint64_t D = c.dim, n = c.n_rows, occ = c.max_occurrences;
+  const uint64_t local = std::max<uint64_t>(dp_rows + flex_rows + rw_rows, 1);
+  f.weights = paged(4 * local * D);
+  f.optimizer_state = c.optimizer == TS_OPT_ROWWISE_ADAGRAD ? paged(4 * local) : 0;
+  f.remap = U > 1 ? paged(n) + paged(4 * n) : 0;
+  // dedup / sort sized for the largest entry count: the batch, plus what
+  // the rank serves for its peers at U > 1
+  const uint64_t recv = U > 1 ? recv_capacity_rows(c) : 0;
+  const uint64_t m = occ + recv;
+  const uint64_t tiles = (m + 4095) / 4096;
+  const uint64_t short_max = U == 1 ? 32 : 256;
+  const uint64_t max_long = m / (short_max + 1) + 1;
+  f.step_buffers = 4 * paged(4 * m)                       // keys / values ping-pong
+                   + paged(8 * 4 * tiles * 512)             // look-back status
+                   + 2 * paged(4 * (m + 1))                 // segment starts + keys
+                   + paged(4 * (2 * ((m + 4095) / 4096) + 4 + ((m + 4095) / 4096 + 4095) / 4096 + 1 + 8))
+                   + paged(4 * max_long) + paged(4 * (max_long + 1))
+                   + paged(4 * (m / 256 + max_long + 1) * D)  // piece partials
+                   + (U > 1 ? 2 * paged(4 * m) : 0);        // (key, source) entries
+  if (U > 1) {
+    f.exchange = 3 * paged(4 * occ)                 // bucket, order, request ids
+                 + paged(4 * recv * D)              // gradient receive buffer
+                 + 2 * paged(4 * recv);             // received ids / positions
+    const uint64_t per_dp = (dp_rows + U - 1) / U;
+    f.replicated = paged(4 * std::max<uint64_t>(U * per_dp, 1) * D) + paged(4 * std::max<uint64_t>(U * per_dp, 1));
+    if (c.num_nodes > 1) {
+      const uint64_t per_flex = (flex_rows + c.num_nodes - 1) / c.num_nodes;
+      f.replicated += paged(4 * std::max<uint64_t>(c.num_nodes * per_flex, 1) * D) +
+                      paged(4 * std::max<uint64_t>(c.num_nodes * per_flex, 1));
+    }
+  }
+  // ts_table_train_step(s)_host: two id buffers and the table-owned output
+  f.host_api = host_api ? 2 * paged(4 * occ) + paged(4 * occ * D) : 0;
+  f.total = f.weights + f.optimizer_state + f.remap + f.step_buffers + f.exchange + f.replicated + f.host_api;
+  return f;
+}
+
+}  // namespace tsd
+
 extern "C" {
+
+ts_status ts_table_plan_footprint(const ts_table_config* cfg, uint64_t dp_rows, uint64_t flex_rows,
+                                  uint64_t rw_rows, int host_api, ts_table_footprint* out) {
+  if (!cfg || !out) {
+    tsd::set_last_error("ts_table_plan_footprint: null argument");
+    return TS_ERR_CONFIG;
+  }
+  if (cfg->num_nodes == 0 || cfg->gpus_per_node == 0 || cfg->dim == 0 || cfg->max_occurrences == 0) {
+    tsd::set_last_error("ts_table_plan_footprint: incomplete configuration");
+    return TS_ERR_CONFIG;
+  }
+  *out = tsd::table_footprint(*cfg, dp_rows, flex_rows, rw_rows, host_api != 0);
+  return TS_OK;
+}
+
 
 ts_status ts_shard_layout(uint64_t n_rows, uint64_t dp_cut, uint64_t flex_cut, const uint8_t* tier_dest,
                           uint32_t num_nodes, uint32_t gpus_per_node, uint32_t rank, uint32_t* local_id,

@@ -31,4 +31,14 @@ struct ExchangePlan {
 // all_starts: [U][U+W+2] bucket starts of every rank.
 void exchange_plan(uint32_t N, uint32_t W, uint32_t g, const uint32_t* all_starts, ExchangePlan* x);
 
+// Gradient receive-buffer capacity (rows) of a U > 1 rank: the caller's
+// recv_rows_hint, else the worst case (every peer's whole batch).
+uint64_t recv_capacity_rows(const ts_table_config& c);
+
+// Device bytes one rank of a table allocates (ts_table_create + the step
+// buffers its entry points size), itemised; mirrors table.cu's allocations,
+// each rounded like DevBuf / dev_alloc (whole 2 MiB pages above 1 MiB).
+ts_table_footprint table_footprint(const ts_table_config& c, uint64_t dp_rows, uint64_t flex_rows,
+                                   uint64_t rw_rows, bool host_api);
+
 }  // namespace tsd

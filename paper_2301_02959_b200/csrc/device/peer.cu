@@ -263,6 +263,14 @@ void* PeerMappings::open(int peer, const IpcExport& e) {
   return static_cast<char*>(it->second.base) + e.offset;
 }
 
+void PeerMappings::close(int peer, const IpcExport& e) {
+  if (direct_) return;
+  auto it = opened_.find(std::make_pair(peer, e.base_id));
+  if (it == opened_.end()) return;
+  cudaIpcCloseMemHandle(it->second.base);
+  opened_.erase(it);
+}
+
 void PeerMappings::close_all() {
   if (std::getenv("TIERSHARD_DEBUG_IPC") && opens_) {
     std::fprintf(stderr, "tiershard: peer mappings: %llu opens, %llu handle changes\n",

@@ -45,6 +45,8 @@ class PeerMappings {
  public:
   // Device pointer (valid in this process) for a peer's export.
   void* open(int peer, const IpcExport& e);
+  // Drops the mapping of a peer allocation that moved (no-op if absent).
+  void close(int peer, const IpcExport& e);
   void close_all();
   void set_direct(bool direct) { direct_ = direct; }
   bool direct() const { return direct_; }

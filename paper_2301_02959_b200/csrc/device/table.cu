@@ -248,7 +248,12 @@ struct ts_table {
   std::vector<const float*> peer_grad;              // peers' gradient buffers (mapped)
   std::vector<float*> peer_dense_dp, peer_dense_flex;  // peers' partial receive buffers (mapped)
   std::vector<uint32_t*> peer_stamp_dp, peer_stamp_flex;  // and their slot stamps
-  std::vector<float*> peer_recv_rows;  // peers' gradient receive buffers (fixed: mapped once)
+  std::vector<float*> peer_recv_rows;  // peers' gradient receive buffers (mapped; moved by regrow_recv)
+  std::vector<uint64_t> peer_recv_cap;  // their capacities, in rows
+  std::vector<tsd::IpcExport> peer_recv_export;
+  uint64_t recv_regrows = 0;
+  void regrow_recv(const std::vector<uint64_t>& need);
+  void exchange_recv_exports();
   uint32_t per_dp = 0, per_flex = 0;  // replicated rows owned per group member
   std::vector<float*> peer_w, peer_state;           // peers' shards (mapped)
   tsd::IpcExport my_export{};                       // staging for the step payload
@@ -476,6 +481,18 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
                              stream));
   }
 
+  {  // fail before allocating when the shard and its step buffers cannot fit
+    const ts_table_footprint fp = table_footprint(c, dp_rows, flex_rows, rw_rows, false);
+    size_t free_b = 0, total_b = 0;
+    TSD_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (fp.total > free_b) {
+      const auto gib = [](uint64_t b) { return std::to_string(static_cast<double>(b) / (1ull << 30)).substr(0, 6); };
+      fail(TS_ERR_CONFIG, "table: rank " + std::to_string(g) + " needs " + gib(fp.total) + " GiB of HBM (weights " +
+                              gib(fp.weights) + ", remap " + gib(fp.remap) + ", step buffers " +
+                              gib(fp.step_buffers) + ", exchange " + gib(fp.exchange) + ") but " + gib(free_b) +
+                              " GiB are free; shard over more GPUs or lower max_occurrences / recv_rows_hint");
+    }
+  }
   TSD_CUDA(dev_alloc(&d_w, sizeof(float) * std::max<uint64_t>(local_rows, 1) * c.dim));
   if (c.optimizer == TS_OPT_ROWWISE_ADAGRAD) {
     TSD_CUDA(dev_alloc(&d_state, sizeof(float) * std::max<uint64_t>(local_rows, 1)));
@@ -522,10 +539,12 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     bucket.ensure(c.max_occurrences);
     order.ensure(c.max_occurrences);
     send_ids.ensure(c.max_occurrences);
-    send_rows.ensure(c.max_occurrences * c.dim);
-    // received gradient rows: peers store into this buffer (P2P push), so it
-    // never moves -- sized once for the worst case, every peer's whole batch
-    recv_rows.ensure(uint64_t{U - 1} * c.max_occurrences * c.dim);
+    // received gradient rows: peers store into this buffer (P2P push), so
+    // it is mapped by every peer and only moves through regrow_recv().
+    // Sized from the caller's hint (the plan's expected remote occurrences
+    // with a margin), else for the worst case, every peer's whole batch
+    // (send_rows, the staged path's buffer, is allocated on first use)
+    recv_rows.ensure(tsd::recv_capacity_rows(c) * c.dim);
     bucket_start.ensure(nb() + 2);
     all_counts.ensure(static_cast<uint64_t>(U) * (nb() + 1));
     // replicated-row gradients: [U][per_dp][D] receive slots (P2P push
@@ -701,6 +720,7 @@ void ts_table::setup_p2p() {
     peer_stamp_flex[p] = static_cast<uint32_t*>(open_opt(e[8]));
     peer_recv_rows[p] = static_cast<float*>(peers.open(pp, e[9]));
   }
+  exchange_recv_exports();
   peer_grad.assign(U, nullptr);
   xfer.ensure(step_payload_bytes() * U);
 }
@@ -710,6 +730,55 @@ void ts_table::setup_p2p() {
 // RW traffic rides `world`; Flex traffic rides `intra` (peer = node slot).
 // The per-peer buffers are laid out [peer p: RW part | Flex part].
 // ---------------------------------------------------------------------------
+
+// Every rank's receive-buffer export and capacity (collective); (re)maps the
+// peers' buffers, closing a peer's previous mapping when it moved.
+void ts_table::exchange_recv_exports() {
+  using namespace tsd;
+  struct Rec {
+    IpcExport e;
+    uint64_t cap_rows;
+  } mine{export_ptr(recv_rows.ptr), recv_rows.cap / cfg.dim};
+  const std::vector<uint8_t> all = allgather_bytes(&mine, sizeof(mine));
+  peer_recv_cap.assign(U, 0);
+  peer_recv_export.resize(U);
+  for (uint32_t p = 0; p < U; ++p) {
+    Rec r;
+    std::memcpy(&r, all.data() + sizeof(Rec) * p, sizeof(Rec));
+    peer_recv_cap[p] = r.cap_rows;
+    if (p == g) continue;
+    const IpcExport& old = peer_recv_export[p];
+    if (old.base_id && (old.base_id != r.e.base_id || std::memcmp(&old.handle, &r.e.handle, sizeof(old.handle)))) {
+      peers.close(static_cast<int>(p), old);
+    }
+    peer_recv_export[p] = r.e;
+    peer_recv_rows[p] = static_cast<float*>(peers.open(static_cast<int>(p), r.e));
+  }
+}
+
+// The checked overflow path of the bounded receive buffers: `need[p]` =
+// rows rank p receives this step (every rank derives the same vector from
+// the all-gathered bucket starts, so all ranks take this path together).  A
+// rank whose capacity is short re-allocates with 25 % headroom; then every
+// rank re-exchanges the exports.  Called after the forward's rendezvous:
+// every peer's previous gradient push into the old buffers has completed
+// (it precedes the previous step's barrier), and our own readers of it are
+// drained here.
+void ts_table::regrow_recv(const std::vector<uint64_t>& need) {
+  using namespace tsd;
+  bool any = false;
+  for (uint32_t p = 0; p < U; ++p) any = any || need[p] > peer_recv_cap[p];
+  if (!any) return;
+  ++recv_regrows;
+  TSD_CUDA(cudaStreamSynchronize(stream));
+  if (aux) TSD_CUDA(cudaStreamSynchronize(aux));
+  TSD_CUDA(cudaStreamSynchronize(comm));
+  if (need[g] > peer_recv_cap[g]) {
+    recv_rows.release();
+    recv_rows.ensure((need[g] + need[g] / 4 + 1) * cfg.dim);
+  }
+  exchange_recv_exports();
+}
 
 void ts_table::group_allreduce(float* buf, uint64_t count, const std::vector<uint32_t>& members,
                                cudaStream_t on) {
@@ -925,6 +994,7 @@ void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   n_local_occ = occ - n_remote;
   recv_ids.ensure(recv_total);
   recv_rows.ensure(recv_total * cfg.dim);
+  send_rows.ensure(std::max<uint64_t>(n_remote, 1) * cfg.dim);
 
   // ---- exchange chain on the comm stream, local gather on the compute
   // stream: the NVLink all-to-allv overlaps the HBM-bound local gather ------
@@ -1200,6 +1270,15 @@ void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   recv_total = xp.recv_total;
   n_remote = xp.n_remote;
   n_local_occ = occ - n_remote;
+  {  // bounded receive buffers: grow (collectively) where this step needs it
+    std::vector<uint64_t> need(U);
+    for (uint32_t p = 0; p < U; ++p) {
+      ExchangePlan pp;
+      exchange_plan(N, W, p, h_counts.data(), &pp);
+      need[p] = pp.recv_total;
+    }
+    regrow_recv(need);
+  }
   recv_ids.ensure(recv_total);
   recv_pos.ensure(recv_total);
 
@@ -1582,6 +1661,14 @@ ts_status ts_table_destroy(ts_table* t) {
     if (!t) return;
     t->destroy();
     delete t;
+  });
+}
+
+ts_status ts_table_recv_capacity(ts_table* t, uint64_t* rows, uint64_t* regrows) {
+  return tsd::guarded([&] {
+    if (!t) tsd::fail(TS_ERR_CONFIG, "ts_table_recv_capacity: null table");
+    if (rows) *rows = t->U > 1 ? t->recv_rows.cap / t->cfg.dim : 0;
+    if (regrows) *regrows = t->recv_regrows;
   });
 }
 

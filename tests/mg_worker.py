@@ -39,7 +39,7 @@ def problem(n_nodes, w, seed=11, steps=1):
                 slot=slot, dest=dest, steps_rows=steps_rows)
 
 
-def rank_body(rank, nodes, w, optimizer, lr, steps, pipelined, device, **table_kw):
+def rank_body(rank, nodes, w, optimizer, lr, steps, pipelined, device, recv_hint=0, **table_kw):
     """One rank's forward + backward (steps == 1, device buffers) or `steps`
     host-buffer steps, through the C-ABI; returns what the parent test
     checks.  table_kw carries the transport: nccl_unique_id (one process per
@@ -52,7 +52,8 @@ def rank_body(rank, nodes, w, optimizer, lr, steps, pipelined, device, **table_k
     table = ts.Table(n_rows=pb["n"], dim=pb["dim"], dp_cut=pb["dp_cut"], flex_cut=pb["flex_cut"],
                      tier_dest=pb["dest"], num_nodes=nodes, gpus_per_node=w,
                      rank=rank, device=device, weight_seed=77, optimizer=optimizer, lr=lr,
-                     max_occurrences=int(max(r[rank].size for r in pb["steps_rows"])), **table_kw)
+                     max_occurrences=int(max(r[rank].size for r in pb["steps_rows"])),
+                     recv_rows_hint=recv_hint, **table_kw)
     if steps > 1:
         if pipelined:
             losses = list(table.train_steps_host([r[rank] for r in pb["steps_rows"]]))
@@ -79,12 +80,12 @@ def rank_body(rank, nodes, w, optimizer, lr, steps, pipelined, device, **table_k
     stored = c[mine].astype(np.uint32)
     wts, st = table.read_rows(stored, with_state=True)
     res = dict(out=out, loss=loss, counters=counters, stored=stored, weights=wts, state=st,
-               shard=np.array(table.shard_rows()))
+               shard=np.array(table.shard_rows()), recv_capacity=np.array(table.recv_capacity()))
     table.close()
     return res
 
 
-def run_inproc(nodes, w, optimizer, lr, steps=1, pipelined=False, env=None):
+def run_inproc(nodes, w, optimizer, lr, steps=1, pipelined=False, env=None, recv_hint=0):
     """All U ranks as threads of this process over one ts_group (rank g on
     GPU g % device_count, so several ranks share a GPU on a small box)."""
     import threading
@@ -101,7 +102,8 @@ def run_inproc(nodes, w, optimizer, lr, steps=1, pipelined=False, env=None):
 
     def body(g):
         try:
-            results[g] = rank_body(g, nodes, w, optimizer, lr, steps, pipelined, g % ndev, group=grp)
+            results[g] = rank_body(g, nodes, w, optimizer, lr, steps, pipelined, g % ndev, recv_hint=recv_hint,
+                                   group=grp)
         except BaseException as e:  # noqa: BLE001 - reported by the caller
             errors[g] = e
 
@@ -132,6 +134,7 @@ def main():
     ap.add_argument("--lr", type=float, default=1e-3)
     ap.add_argument("--steps", type=int, default=1, help="> 1: host-buffer steps (train_step_host)")
     ap.add_argument("--pipelined", action="store_true", help="the steps in one train_steps_host call")
+    ap.add_argument("--recv-hint", type=int, default=0, help="recv_rows_hint (tiny: forces regrowth)")
     ap.add_argument("--out", required=True)
     args = ap.parse_args()
     import torch.distributed as td
@@ -145,7 +148,7 @@ def main():
     box = [ts.nccl_unique_id() if rank == 0 else None]
     td.broadcast_object_list(box, src=0)
     res = rank_body(rank, args.nodes, args.gpus_per_node, args.optimizer, args.lr, args.steps,
-                    args.pipelined, local, nccl_unique_id=box[0])
+                    args.pipelined, local, recv_hint=args.recv_hint, nccl_unique_id=box[0])
     np.savez(Path(args.out) / f"rank{rank}.npz", **res)
     td.barrier()
     td.destroy_process_group()

@@ -11,8 +11,16 @@ across ranks.
 The 1e-6 bar (north star) applies at a training-scale learning rate: the
 all-reduce sums a replicated row's gradient in a different fp32 order than the
 single-process oracle (~sqrt(n) ulps apart for n occurrences), and that
-difference reaches the weight scaled by lr * |step| / |w|."""
-LR = 1e-3
+difference reaches the weight scaled by lr * |step| / |w|.  The global batch
+grows with U (the hottest row gets ~1800 occurrences per 2 ranks), so the
+rate is 2e-3 / U: lr x (hottest row's count) stays ~1.8 at every U rather
+than flipping that row's sign several times over at U = 8."""
+
+
+def lr_for(u):
+    return 2e-3 / u
+
+
 # multi-step runs feed each step's weights into the next step's gradients
 # (grad = out); a smaller rate keeps SGD on the hottest rows contractive so the
 # summation-order differences do not compound across steps
@@ -64,7 +72,8 @@ def run_ranks(u, worker_args, env=None):
 CASES = [(1, 2, 1, "p2p"), (2, 1, 1, "p2p"), (2, 1, 0, "p2p"), (2, 2, 1, "p2p"), (1, 4, 1, "p2p"),
          (1, 2, 1, "p2p_pull"), (2, 2, 1, "p2p_pull"), (1, 4, 0, "p2p_pull"),
          (1, 2, 1, "nccl"), (2, 2, 1, "nccl"), (2, 1, 0, "nccl"),
-         (1, 2, 1, "p2p_short8"), (2, 2, 1, "p2p_short8"), (1, 2, 1, "p2p_serial")]
+         (1, 2, 1, "p2p_short8"), (2, 2, 1, "p2p_short8"), (1, 2, 1, "p2p_serial"),
+         (1, 2, 1, "p2p_regrow"), (2, 2, 0, "p2p_regrow")]
 # always in-process (ts_group): the C2 topologies at logical U = 8 on however
 # many GPUs the box has (several ranks per GPU), and a 2-per-GPU mix
 INPROC_CASES = [(1, 8, 1, "p2p"), (2, 4, 1, "p2p"), (2, 4, 0, "nccl"), (1, 3, 1, "p2p"), (3, 2, 1, "p2p_pull")]
@@ -79,7 +88,8 @@ def case_env(exchange):
     return env
 
 
-def run_case(tmp_path, n_nodes, w, opt, lr, exchange="p2p", steps=1, pipelined=False, transport="auto"):
+def run_case(tmp_path, n_nodes, w, opt, lr, exchange="p2p", steps=1, pipelined=False, transport="auto",
+             recv_hint=0):
     """Runs every rank and returns their results.  transport "auto": one
     process per GPU (NCCL + CUDA IPC) when the box has U GPUs, else all ranks
     as threads of this process over a ts_group (several ranks per GPU) --
@@ -87,14 +97,17 @@ def run_case(tmp_path, n_nodes, w, opt, lr, exchange="p2p", steps=1, pipelined=F
     small box.  "inproc" forces the group."""
     u = n_nodes * w
     env = case_env(exchange)
+    if exchange == "p2p_regrow":
+        recv_hint = 16  # far below one step's remote rows: the first step regrows
     if transport == "auto" and n_devices() >= u:
         args = ["--nodes", str(n_nodes), "--gpus-per-node", str(w), "--optimizer", str(opt), "--lr", str(lr),
-                "--steps", str(steps), "--out", str(tmp_path)] + (["--pipelined"] if pipelined else [])
+                "--steps", str(steps), "--recv-hint", str(recv_hint), "--out", str(tmp_path)] + \
+               (["--pipelined"] if pipelined else [])
         proc = run_ranks(u, args, dict(os.environ, **env))
         assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
         return [dict(np.load(tmp_path / f"rank{g}.npz")) for g in range(u)]
     print(f"in-process group: {u} ranks on {max(1, n_devices())} GPU(s)")
-    return mg_worker.run_inproc(n_nodes, w, opt, lr, steps=steps, pipelined=pipelined, env=env)
+    return mg_worker.run_inproc(n_nodes, w, opt, lr, steps=steps, pipelined=pipelined, env=env, recv_hint=recv_hint)
 
 
 def assert_rows_close(got, ref, before, rtol=1e-6):
@@ -115,7 +128,7 @@ def assert_rows_close(got, ref, before, rtol=1e-6):
     assert not bad.any(), (int(bad.sum()), float((np.abs(got - ref) / np.maximum(scale, 1e-30)).max()))
 
 
-def check_one_step(res, n_nodes, w, opt):
+def check_one_step(res, n_nodes, w, opt, lr):
     """forward bit-exact, counters == the reference loop, updates == oracle."""
     u = n_nodes * w
     pb = mg_worker.problem(n_nodes, w)
@@ -138,7 +151,7 @@ def check_one_step(res, n_nodes, w, opt):
     # backward: oracle over the concatenated global batch (ascending rank order)
     w_ref = w0.copy()
     st_ref = np.zeros(n, np.float32)
-    orc.backward_update(w_ref, st_ref, allrows, orc.gather(w0, allrows), opt, LR, 1e-8)
+    orc.backward_update(w_ref, st_ref, allrows, orc.gather(w0, allrows), opt, lr, 1e-8)
     for g in range(u):
         stored = res[g]["stored"]
         got = res[g]["weights"]
@@ -160,9 +173,14 @@ def test_multi_gpu_matches_oracle(cuda, tmp_path, n_nodes, w, opt, exchange):
     (TIERSHARD_EXCHANGE=nccl; NCCL between processes, the group's copies and
     sum kernel in-process), "p2p_short8" = segments over 8 entries take the
     piece path on the aux stream (TIERSHARD_SHORT_MAX=8), "p2p_serial" = long
-    segments after the short kernel (TIERSHARD_LONG_CONCURRENT=0)."""
-    res = run_case(tmp_path, n_nodes, w, opt, LR, exchange)
-    check_one_step(res, n_nodes, w, opt)
+    segments after the short kernel (TIERSHARD_LONG_CONCURRENT=0),
+    "p2p_regrow" = a 16-row gradient receive buffer (recv_rows_hint): the
+    step takes the collective regrowth path first."""
+    res = run_case(tmp_path, n_nodes, w, opt, lr_for(n_nodes * w), exchange)
+    check_one_step(res, n_nodes, w, opt, lr_for(n_nodes * w))
+    if exchange == "p2p_regrow":  # the path was taken, collectively
+        assert all(int(r["recv_capacity"][1]) >= 1 for r in res)
+        assert any(int(r["recv_capacity"][0]) > 16 for r in res)
 
 
 @pytest.mark.parametrize("n_nodes,w,opt,exchange", INPROC_CASES)
@@ -170,20 +188,26 @@ def test_inproc_group_matches_oracle(cuda, tmp_path, n_nodes, w, opt, exchange):
     """Every rank a thread of this process over one ts_group: logical U = 8
     (1x8 2-tier, 2x4 3-tier -- the C2 topologies), odd shapes, on however many
     GPUs the box has."""
-    res = run_case(tmp_path, n_nodes, w, opt, LR, exchange, transport="inproc")
-    check_one_step(res, n_nodes, w, opt)
+    res = run_case(tmp_path, n_nodes, w, opt, lr_for(n_nodes * w), exchange, transport="inproc")
+    check_one_step(res, n_nodes, w, opt, lr_for(n_nodes * w))
 
 
-@pytest.mark.parametrize("n_nodes,w,opt,pipelined", [(1, 2, 1, False), (2, 2, 1, False), (1, 4, 0, False),
-                                                     (1, 2, 1, True), (2, 2, 1, True)])
-def test_multi_gpu_host_steps_match_oracle(cuda, tmp_path, n_nodes, w, opt, pipelined):
+@pytest.mark.parametrize("n_nodes,w,opt,pipelined,hint", [(1, 2, 1, False, 0), (2, 2, 1, False, 0),
+                                                          (1, 4, 0, False, 0), (1, 2, 1, True, 0),
+                                                          (2, 2, 1, True, 0), (1, 2, 1, True, 2000),
+                                                          (2, 2, 0, False, 2000)])
+def test_multi_gpu_host_steps_match_oracle(cuda, tmp_path, n_nodes, w, opt, pipelined, hint):
     """Three steps through the host-buffer entry point (ts_table_train_step_host)
     with batches growing step to step: every step's loss and the final weights
     follow the oracle's sequential updates (stale peer mappings or stale
     replica stamps would break this)."""
     u = n_nodes * w
     steps = 3
-    res = run_case(tmp_path, n_nodes, w, opt, LR_STEPS, steps=steps, pipelined=pipelined)
+    # hint 2000: the receive buffer starts below a step's need and grows
+    # step to step as the batches grow (peers re-map it each time)
+    res = run_case(tmp_path, n_nodes, w, opt, LR_STEPS, steps=steps, pipelined=pipelined, recv_hint=hint)
+    if hint:
+        assert all(int(r["recv_capacity"][1]) >= 1 for r in res)
     pb = mg_worker.problem(n_nodes, w, steps=steps)
     n, dim, dp, fx = pb["n"], pb["dim"], pb["dp_cut"], pb["flex_cut"]
     w_ref = orc.init_table(77, n, dim)
