@@ -194,8 +194,8 @@ def test_inproc_group_matches_oracle(cuda, tmp_path, n_nodes, w, opt, exchange):
 
 @pytest.mark.parametrize("n_nodes,w,opt,pipelined,hint", [(1, 2, 1, False, 0), (2, 2, 1, False, 0),
                                                           (1, 4, 0, False, 0), (1, 2, 1, True, 0),
-                                                          (2, 2, 1, True, 0), (1, 2, 1, True, 2000),
-                                                          (2, 2, 0, False, 2000)])
+                                                          (2, 2, 1, True, 0), (1, 2, 1, True, 600),
+                                                          (2, 2, 0, False, 600)])
 def test_multi_gpu_host_steps_match_oracle(cuda, tmp_path, n_nodes, w, opt, pipelined, hint):
     """Three steps through the host-buffer entry point (ts_table_train_step_host)
     with batches growing step to step: every step's loss and the final weights
@@ -203,7 +203,7 @@ def test_multi_gpu_host_steps_match_oracle(cuda, tmp_path, n_nodes, w, opt, pipe
     replica stamps would break this)."""
     u = n_nodes * w
     steps = 3
-    # hint 2000: the receive buffer starts below a step's need and grows
+    # hint 600: the receive buffer starts below a step's need and grows
     # step to step as the batches grow (peers re-map it each time)
     res = run_case(tmp_path, n_nodes, w, opt, LR_STEPS, steps=steps, pipelined=pipelined, recv_hint=hint)
     if hint:
