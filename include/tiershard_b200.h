@@ -248,6 +248,9 @@ typedef struct ts_table ts_table;
  * call and poisons the group).  Destroy the group after its tables. */
 typedef struct ts_group ts_group;
 ts_status ts_group_create(ts_group** out, uint32_t ranks);
+/* Marks the group failed (a rank's host thread failed outside the library):
+ * every pending and later collective of its tables returns an error at once. */
+ts_status ts_group_abort(ts_group* g);
 ts_status ts_group_destroy(ts_group* g);
 
 typedef struct ts_table_config {

@@ -80,6 +80,7 @@ EXPORTS = (
     "ts_frontier_preview",
     "ts_group_create",
     "ts_group_destroy",
+    "ts_group_abort",
     "ts_table_plan_footprint",
     "ts_table_recv_capacity",
 )
@@ -183,6 +184,7 @@ def load() -> C.CDLL:
         "ts_frontier_preview": (C.c_int, [C.c_int, C.c_uint64, vp, C.c_uint32, vp, vp]),
         "ts_group_create": (C.c_int, [C.POINTER(vp), C.c_uint32]),
         "ts_group_destroy": (C.c_int, [vp]),
+        "ts_group_abort": (C.c_int, [vp]),
         "ts_table_recv_capacity": (C.c_int, [vp, u64p, u64p]),
         "ts_table_plan_footprint": (C.c_int, [C.POINTER(TableConfig), C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
                                               C.POINTER(Footprint)]),
@@ -394,6 +396,10 @@ class Group:
     @property
     def handle(self) -> int:
         return self._h.value
+
+    def abort(self) -> None:
+        """A rank's thread failed: every pending collective fails at once."""
+        _check(self._lib.ts_group_abort(self._h))
 
     def close(self):
         if getattr(self, "_h", None):

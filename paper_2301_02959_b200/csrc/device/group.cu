@@ -89,6 +89,13 @@ void group_allgather(ts_group* g, uint32_t rank, const void* mine, size_t bytes,
   wait_locked(g, lk);  // every rank has read: the buffer may be reused
 }
 
+void group_poison(ts_group* g) {
+  if (!g) return;
+  std::lock_guard<std::mutex> lk(g->mu);
+  g->broken = true;
+  g->cv.notify_all();
+}
+
 void group_barrier(ts_group* g, uint32_t rank, cudaStream_t stream) {
   std::unique_lock<std::mutex> lk(g->mu);
   const uint64_t k = g->seq[rank]++;
@@ -117,6 +124,13 @@ ts_status ts_group_create(ts_group** out, uint32_t ranks) {
       g->timeout = std::chrono::seconds(std::max(1, std::atoi(e)));
     }
     *out = g;
+  });
+}
+
+ts_status ts_group_abort(ts_group* g) {
+  return tsd::guarded([&] {
+    if (!g) tsd::fail(TS_ERR_CONFIG, "ts_group_abort: null group");
+    tsd::group_poison(g);
   });
 }
 

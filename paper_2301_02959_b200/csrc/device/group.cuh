@@ -46,5 +46,8 @@ void group_wait(ts_group* g);
 void group_allgather(ts_group* g, uint32_t rank, const void* mine, size_t bytes, void* all);
 // Device rendezvous on `stream` (see above).
 void group_barrier(ts_group* g, uint32_t rank, cudaStream_t stream);
+// Marks the group unusable (a rank failed): every pending and later
+// rendezvous fails at once.
+void group_poison(ts_group* g);
 
 }  // namespace tsd

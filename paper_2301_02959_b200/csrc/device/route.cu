@@ -110,8 +110,10 @@ build_entries_kernel(const uint32_t* __restrict__ rows, const uint32_t* __restri
 
 __global__ void bucket_starts_kernel(const uint32_t* __restrict__ hist_scan, uint64_t tiles,
                                      uint32_t nb, uint32_t occ, uint32_t* __restrict__ out) {
+  // an empty batch is not sorted at all (hist_scan holds a previous batch's
+  // offsets): every bucket starts at 0
   for (uint32_t b = threadIdx.x; b <= nb; b += blockDim.x) {
-    out[b] = b < nb ? hist_scan[static_cast<uint64_t>(b) * tiles] : occ;
+    out[b] = b < nb && occ ? hist_scan[static_cast<uint64_t>(b) * tiles] : occ;
   }
 }
 

@@ -534,8 +534,14 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
   nseg.ensure(4);
   seg_split.ensure(4);
   long_count.ensure(4);
-  ensure_sort_capacity(c.max_occurrences);
+  // dedup / sort sized once for the largest entry count a step can have
+  // (the batch, plus what this rank serves at U > 1): a DevBuf that grows
+  // mid-run frees and re-allocates, which synchronises the device
+  const uint64_t max_entries = c.max_occurrences + (U > 1 ? recv_capacity_rows(c) : 0);
+  ensure_sort_capacity(max_entries);
   if (U > 1) {
+    entry_keys.ensure(max_entries);
+    entry_vals.ensure(max_entries);
     bucket.ensure(c.max_occurrences);
     order.ensure(c.max_occurrences);
     send_ids.ensure(c.max_occurrences);
@@ -886,6 +892,11 @@ void ts_table::dedup_p2p(cudaStream_t on) {
   segment_starts(dd_keys, m, starts.ptr, seg_keys.ptr, nseg.ptr, seg_scratch.ptr, on);
   const uint32_t dense_hi = static_cast<uint32_t>(dp_rows + (N > 1 ? flex_rows : 0));
   launch_segment_split(dd_keys, starts.ptr, nseg.ptr, dense_hi, seg_split.ptr, on);
+  // several nodes: the DP segments end inside the replicated range, at
+  // seg_split[3] (their entries are all local, see backward_p2p)
+  if (N > 1 && flex_rows) {
+    launch_segment_split(dd_keys, starts.ptr, nseg.ptr, static_cast<uint32_t>(dp_rows), seg_split.ptr + 2, on);
+  }
   phase_end(t);
 }
 
@@ -1481,23 +1492,31 @@ void ts_table::backward_p2p(const float* d_grad) {
   gs.n_local = static_cast<uint32_t>(occ);
   gs.remote = recv_rows.ptr;
 
-  // ---- replicated rows first; their reduction overlaps the RW updates.  With
-  // one node the replicated (DP) segments hold local entries only and start
-  // without the remote rows; Flex rows replicated across nodes need them.
-  const bool dense_needs_remote = N > 1 && flex_rows;
-  if (dense_needs_remote) TSD_CUDA(cudaStreamWaitEvent(stream, ev_grads, 0));
-  if (long_concurrent) {
-    segment_range_concurrent(sk, sv, seg_split.ptr, seg_split.ptr + 1, m, gs, opt, d0, d1);
-  } else {
-    t = phase_begin(kPhaseSegmentUpdate);
-    launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, seg_split.ptr, seg_split.ptr + 1, m, cfg.dim, gs, d_w,
-                          d_state, opt, d0, d1, sc, stream);
-    phase_end(t);
-    t = phase_begin(kPhaseSegmentLong);
+  // ---- replicated rows first; their reduction overlaps the RW updates.  The
+  // DP segments hold local entries only (a DP row is served by its
+  // requester), so they start without the remote rows, beside the gradient
+  // push; Flex rows replicated across nodes (N > 1) need them.
+  const auto seg_range = [&](const uint32_t* d_lo, const uint32_t* d_hi) {
+    if (long_concurrent) {
+      segment_range_concurrent(sk, sv, d_lo, d_hi, m, gs, opt, d0, d1);
+      return;
+    }
+    int tt = phase_begin(kPhaseSegmentUpdate);
+    launch_segment_update(sk, sv, starts.ptr, seg_keys.ptr, d_lo, d_hi, m, cfg.dim, gs, d_w, d_state, opt, d0, d1,
+                          sc, stream);
+    phase_end(tt);
+    tt = phase_begin(kPhaseSegmentLong);
     launch_segment_long(sk, sv, starts.ptr, m, cfg.dim, gs, d_w, d_state, opt, d0, d1, sc, stream);
-    phase_end(t);
+    phase_end(tt);
+  };
+  if (N > 1 && flex_rows) {
+    seg_range(seg_split.ptr + 2, seg_split.ptr + 3);  // DP: [0, split at dp_rows)
+    TSD_CUDA(cudaStreamWaitEvent(stream, ev_grads, 0));
+    seg_range(seg_split.ptr + 3, seg_split.ptr + 1);  // Flex: up to the replicated bound
+  } else {
+    seg_range(seg_split.ptr, seg_split.ptr + 1);
+    TSD_CUDA(cudaStreamWaitEvent(stream, ev_grads, 0));
   }
-  if (!dense_needs_remote) TSD_CUDA(cudaStreamWaitEvent(stream, ev_grads, 0));
   // ---- replicated tiers over peer memory: after a rendezvous (all ranks'
   // partials written), each rank reduces its slice of the replicated rows in
   // group-rank order, updates it and broadcasts it to every replica --------
@@ -1638,6 +1657,18 @@ void ts_table::destroy() {
 // C-ABI
 // ---------------------------------------------------------------------------
 
+namespace {
+// guarded() for the entry points of a table that may sit in an in-process
+// group: a failure poisons the group, so the other ranks' collectives fail
+// at once instead of waiting out the rendezvous timeout.
+template <typename Body>
+ts_status table_guarded(ts_table* t, Body&& body) {
+  const ts_status st = tsd::guarded(std::forward<Body>(body));
+  if (st != TS_OK && t && t->grp) tsd::group_poison(t->grp);
+  return st;
+}
+}  // namespace
+
 extern "C" {
 
 ts_status ts_table_create(ts_table** out, const ts_table_config* cfg, const uint8_t* tier_dest) {
@@ -1649,6 +1680,7 @@ ts_status ts_table_create(ts_table** out, const ts_table_config* cfg, const uint
       t->create(*cfg, tier_dest);
       t->ready = true;
     } catch (...) {
+      if (cfg->group) tsd::group_poison(cfg->group);  // the other ranks' creation fails fast
       t->destroy();
       throw;
     }
@@ -1689,7 +1721,7 @@ ts_status ts_table_stream(ts_table* t, void** stream) {
 }
 
 ts_status ts_table_forward(ts_table* t, const uint32_t* d_rows, uint64_t occ, float* d_out) {
-  return tsd::guarded([&] {
+  return table_guarded(t, [&] {
     if (!t || (occ && (!d_rows || !d_out))) tsd::fail(TS_ERR_CONFIG, "ts_table_forward: null argument");
     TSD_CUDA(cudaSetDevice(t->cfg.device));
     t->forward(d_rows, occ, d_out);
@@ -1697,7 +1729,7 @@ ts_status ts_table_forward(ts_table* t, const uint32_t* d_rows, uint64_t occ, fl
 }
 
 ts_status ts_table_backward(ts_table* t, const float* d_grad) {
-  return tsd::guarded([&] {
+  return table_guarded(t, [&] {
     if (!t || (t->last_occ && !d_grad)) tsd::fail(TS_ERR_CONFIG, "ts_table_backward: null argument");
     TSD_CUDA(cudaSetDevice(t->cfg.device));
     t->backward(d_grad);
@@ -1705,7 +1737,7 @@ ts_status ts_table_backward(ts_table* t, const float* d_grad) {
 }
 
 ts_status ts_table_train_step(ts_table* t, const uint32_t* d_rows, uint64_t occ, float* d_out) {
-  return tsd::guarded([&] {
+  return table_guarded(t, [&] {
     if (!t || (occ && (!d_rows || !d_out))) tsd::fail(TS_ERR_CONFIG, "ts_table_train_step: null argument");
     TSD_CUDA(cudaSetDevice(t->cfg.device));
     t->forward(d_rows, occ, d_out);
@@ -1714,7 +1746,7 @@ ts_status ts_table_train_step(ts_table* t, const uint32_t* d_rows, uint64_t occ,
 }
 
 ts_status ts_table_train_step_host(ts_table* t, const uint32_t* h_rows, uint64_t occ, double* h_loss) {
-  return tsd::guarded([&] {
+  return table_guarded(t, [&] {
     if (!t || (occ && !h_rows)) tsd::fail(TS_ERR_CONFIG, "ts_table_train_step_host: null argument");
     TSD_CUDA(cudaSetDevice(t->cfg.device));
     if (occ > t->cfg.max_occurrences) {
@@ -1739,7 +1771,7 @@ ts_status ts_table_train_step_host(ts_table* t, const uint32_t* h_rows, uint64_t
 
 ts_status ts_table_train_steps_host(ts_table* t, const uint32_t* const* h_rows, const uint64_t* occ,
                                    uint32_t steps, double* h_losses) {
-  return tsd::guarded([&] {
+  return table_guarded(t, [&] {
     using namespace tsd;
     if (!t || (steps && (!h_rows || !occ))) tsd::fail(TS_ERR_CONFIG, "ts_table_train_steps_host: null argument");
     TSD_CUDA(cudaSetDevice(t->cfg.device));
@@ -1912,7 +1944,7 @@ ts_status ts_table_read_rows(ts_table* t, const uint32_t* rows, uint64_t count, 
 }
 
 ts_status ts_table_synchronize(ts_table* t) {
-  return tsd::guarded([&] {
+  return table_guarded(t, [&] {
     if (!t) tsd::fail(TS_ERR_CONFIG, "ts_table_synchronize: null table");
     TSD_CUDA(cudaSetDevice(t->cfg.device));
     if (t->p2p) {

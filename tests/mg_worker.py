@@ -17,10 +17,12 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
 
-def problem(n_nodes, w, seed=11, steps=1):
+def problem(n_nodes, w, seed=11, steps=1, varying=False):
     """rows[g] is rank g's first batch; steps > 1 adds steps_rows[s][g] for
     the host-API multi-step case, batches growing step to step (so any
-    per-step buffer sized by the batch would have to move)."""
+    per-step buffer sized by the batch would have to move).  varying: ragged
+    batches instead -- every step a random size in [0, 6000) per rank, with
+    empty batches on rank 0 at step 7 and on every rank at step 11."""
     import oracle_bind as orc
     u = n_nodes * w
     n, dim = 12000, 64
@@ -31,7 +33,15 @@ def problem(n_nodes, w, seed=11, steps=1):
     rows = [rng.choice(n, size=o, p=p / p.sum()).astype(np.uint32) for o in occ]
     steps_rows = [rows]
     for s in range(1, steps):
-        steps_rows.append([rng.choice(n, size=o + 1500 * s, p=p / p.sum()).astype(np.uint32) for o in occ])
+        if varying:
+            sizes = [int(x) for x in rng.integers(0, 6000, size=u)]
+            if s == 7:
+                sizes[0] = 0
+            if s == 11:
+                sizes = [0] * u
+        else:
+            sizes = [o + 1500 * s for o in occ]
+        steps_rows.append([rng.choice(n, size=o, p=p / p.sum()).astype(np.uint32) for o in sizes])
     tier, owner, slot = orc.assign_rows(np.zeros(n, np.uint32), np.arange(n, dtype=np.uint64),
                                         dp_cut, flex_cut, u, w, 2)
     dest = np.where(tier == 1, slot, owner).astype(np.uint8)
@@ -39,7 +49,7 @@ def problem(n_nodes, w, seed=11, steps=1):
                 slot=slot, dest=dest, steps_rows=steps_rows)
 
 
-def rank_body(rank, nodes, w, optimizer, lr, steps, pipelined, device, recv_hint=0, **table_kw):
+def rank_body(rank, nodes, w, optimizer, lr, steps, pipelined, device, recv_hint=0, varying=False, **table_kw):
     """One rank's forward + backward (steps == 1, device buffers) or `steps`
     host-buffer steps, through the C-ABI; returns what the parent test
     checks.  table_kw carries the transport: nccl_unique_id (one process per
@@ -48,7 +58,7 @@ def rank_body(rank, nodes, w, optimizer, lr, steps, pipelined, device, recv_hint
     import paper_2301_02959_b200 as ts
 
     torch.cuda.set_device(device)
-    pb = problem(nodes, w, steps=steps)
+    pb = problem(nodes, w, steps=steps, varying=varying)
     table = ts.Table(n_rows=pb["n"], dim=pb["dim"], dp_cut=pb["dp_cut"], flex_cut=pb["flex_cut"],
                      tier_dest=pb["dest"], num_nodes=nodes, gpus_per_node=w,
                      rank=rank, device=device, weight_seed=77, optimizer=optimizer, lr=lr,
@@ -85,7 +95,7 @@ def rank_body(rank, nodes, w, optimizer, lr, steps, pipelined, device, recv_hint
     return res
 
 
-def run_inproc(nodes, w, optimizer, lr, steps=1, pipelined=False, env=None, recv_hint=0):
+def run_inproc(nodes, w, optimizer, lr, steps=1, pipelined=False, env=None, recv_hint=0, varying=False):
     """All U ranks as threads of this process over one ts_group (rank g on
     GPU g % device_count, so several ranks share a GPU on a small box)."""
     import threading
@@ -103,9 +113,10 @@ def run_inproc(nodes, w, optimizer, lr, steps=1, pipelined=False, env=None, recv
     def body(g):
         try:
             results[g] = rank_body(g, nodes, w, optimizer, lr, steps, pipelined, g % ndev, recv_hint=recv_hint,
-                                   group=grp)
+                                   varying=varying, group=grp)
         except BaseException as e:  # noqa: BLE001 - reported by the caller
             errors[g] = e
+            grp.abort()  # the other ranks' collectives fail now, not at the timeout
 
     try:
         threads = [threading.Thread(target=body, args=(g,)) for g in range(u)]

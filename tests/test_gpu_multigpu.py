@@ -223,3 +223,34 @@ def test_multi_gpu_host_steps_match_oracle(cuda, tmp_path, n_nodes, w, opt, pipe
         np.testing.assert_allclose(res[g]["weights"], w_ref[stored], rtol=1e-6, atol=1e-8)
     for g in range(1, u):
         assert np.array_equal(res[g]["weights"][:dp].view(np.uint32), res[0]["weights"][:dp].view(np.uint32))
+
+
+@pytest.mark.parametrize("n_nodes,w,pipelined", [(1, 2, True), (2, 2, False)])
+def test_inproc_stress_ragged_steps(cuda, tmp_path, n_nodes, w, pipelined):
+    """50 host-buffer steps with ragged batches (random sizes, an empty batch
+    on one rank, an all-empty step) through the peer-memory protocol on the
+    in-process group, a tiny initial receive buffer (regrowth mid-run):
+    every step's loss and the final weights / Adagrad state follow the
+    oracle's 50 sequential updates; replicas stay identical."""
+    u, steps = n_nodes * w, 50
+    res = mg_worker.run_inproc(n_nodes, w, 1, LR_STEPS, steps=steps, pipelined=pipelined, recv_hint=64,
+                               varying=True)
+    pb = mg_worker.problem(n_nodes, w, steps=steps, varying=True)
+    n, dim, dp = pb["n"], pb["dim"], pb["dp_cut"]
+    w_ref = orc.init_table(77, n, dim)
+    w0 = w_ref.copy()
+    st_ref = np.zeros(n, np.float32)
+    for s, batch in enumerate(pb["steps_rows"]):
+        allrows = np.concatenate(batch)
+        for g in range(u):
+            expect = orc.half_sq_sum(orc.gather(w_ref, batch[g]))
+            assert float(res[g]["loss"][s]) == pytest.approx(expect, rel=1e-6, abs=1e-12), (s, g)
+        if allrows.size:
+            orc.backward_update(w_ref, st_ref, allrows, orc.gather(w_ref, allrows), 1, LR_STEPS, 1e-8)
+    for g in range(u):
+        stored = res[g]["stored"]
+        assert_rows_close(res[g]["weights"], w_ref[stored], w0[stored])
+        np.testing.assert_allclose(res[g]["state"], st_ref[stored], rtol=1e-5, atol=1e-12)
+        assert int(res[g]["recv_capacity"][1]) >= 1
+    for g in range(1, u):
+        assert np.array_equal(res[g]["weights"][:dp].view(np.uint32), res[0]["weights"][:dp].view(np.uint32))
