@@ -276,7 +276,21 @@ def ncu_traffic(phase, u):
     entry = doc.get("n1" if u == 1 else f"n{u}", {}).get(phase)
     if not entry:
         return None, None
-    return entry["dram_bytes_per_step"], doc.get("source")
+    return entry["dram_bytes_per_step"], entry.get("source", doc.get("source"))
+
+
+def ncu_nvlink(u):
+    """Per-kernel NVLink payload rates of the exchange kernels running alone
+    (profiles/r02_ncu_nvlink_n<U>.json, tools/ncu_nvlink.sh), or None."""
+    try:
+        doc = json.loads((ROOT / "profiles" / f"r02_ncu_nvlink_n{u}.json").read_text())
+    except Exception:
+        return None
+    keep = ("serve_rows_kernel", "void push_grads_kernel", "replica_update_kernel", "seg_short_kernel (replicated range)")
+    return {"source": doc["source"],
+            "kernels": {k.replace("void ", ""): {"nvlink_user_tx_gbs": v["nvlink_user_tx_gbs"],
+                                                 "nvltx_user_bytes": v["nvltx_user_bytes"], "avg_time_us": v["avg_time_us"]}
+                        for k, v in doc["per_kernel"].items() if k in keep}}
 
 
 def measured_peaks():
@@ -681,7 +695,7 @@ def run_ours(args, dist: Dist):
         peer_peak, peak_src = nvlink_peak(p2p_ceiling)
         nvlink = {"bytes_per_gpu_per_step": total, "breakdown": per_gpu,
                   "achieved_gbs": round(total / step_s / 1e9, 1), "peak_gbs": peer_peak,
-                  "peak_source": peak_src, "p2p_ceiling": p2p_ceiling,
+                  "peak_source": peak_src, "p2p_ceiling": p2p_ceiling, "ncu_alone": ncu_nvlink(u),
                   "frac": round(total / step_s / 1e9 / peer_peak, 4),
                   "bound_ms": round(total / (peer_peak * 1e9) * 1e3, 4)}
 
