@@ -147,6 +147,163 @@ gather_local_kernel(const uint32_t* __restrict__ rows, uint64_t occ,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Bulk-copy gather (TIERSHARD_GATHER=bulk): the same contract as
+// gather_local_kernel, with the rows moved by the copy engine instead of
+// registers.  Each warp owns a ring of kBulkStages shared-memory stages of
+// 4 KB; one elected lane issues cp.async.bulk global->shared loads of a
+// stage's rows (one 16-B-aligned row each), completing on the stage's
+// mbarrier, then ONE cp.async.bulk shared->global store of the stage when
+// its rows are consecutive in `out` (always at U = 1), else one per row.
+// The lanes only read the stage once for the loss partial.  Loads of
+// kBulkStages - 1 stages stay in flight behind each store.
+// ---------------------------------------------------------------------------
+
+constexpr int kBulkThreads = 128;
+constexpr int kBulkMaxStages = 8;
+constexpr uint32_t kBulkStageBytes = 4096;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+template <int DIM>
+__global__ void __launch_bounds__(kBulkThreads)
+gather_bulk_kernel(const uint32_t* __restrict__ rows, uint64_t occ, const float* __restrict__ weights,
+                   float* __restrict__ out, RemapView rv, double* __restrict__ loss_partials, int kBulkStages) {
+  constexpr uint32_t kRowBytes = DIM * 4;
+  constexpr int R = kBulkStageBytes / kRowBytes;  // rows per stage (<= 32)
+  static_assert(R >= 1 && R <= 32, "stage holds 1..32 rows");
+  constexpr int kWarps = kBulkThreads / 32;
+  extern __shared__ __align__(128) uint8_t bulk_smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bulk_smem);  // [kWarps][kBulkMaxStages]
+  uint8_t* stages = bulk_smem + 8 * kWarps * kBulkMaxStages;  // [kWarps][kBulkStages][4 KB]
+  __shared__ float s_sq[kWarps];
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint64_t* my_bars = bars + warp * kBulkMaxStages;
+  uint8_t* my_stages = stages + static_cast<size_t>(warp) * kBulkStages * kBulkStageBytes;
+  if (lane == 0) {
+    for (int st = 0; st < kBulkStages; ++st) mbar_init(my_bars + st, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncwarp();
+  const uint64_t gwarp = static_cast<uint64_t>(blockIdx.x) * kWarps + warp;
+  const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * kWarps;
+  const uint64_t groups = (occ + R - 1) / R;
+  // group j of this warp = global group gwarp + j * nwarps
+  uint32_t ok_mask[kBulkMaxStages];  // valid local rows of the group in each stage (lane 0)
+  const auto issue = [&](uint64_t j, int st) {
+    const uint64_t gi = gwarp + j * nwarps;
+    uint32_t lid = 0;
+    bool ok = false;
+    const uint64_t i = gi * R + lane;
+    if (gi < groups && lane < static_cast<unsigned>(R) && i < occ) ok = resolve_local(rv, __ldg(rows + i), &lid);
+    const uint32_t mask = __ballot_sync(0xFFFFFFFFu, ok);
+    if (lane == 0) {
+      ok_mask[st] = mask;
+      mbar_expect_tx(my_bars + st, __popc(mask) * kRowBytes);
+    }
+    __syncwarp();
+    // each valid lane issues its own row's copy (lanes >= R never valid)
+    if (ok) {
+      bulk_load(my_stages + st * kBulkStageBytes + lane * kRowBytes, weights + static_cast<uint64_t>(lid) * DIM,
+                kRowBytes, my_bars + st);
+    }
+  };
+  const uint64_t my_groups = gwarp < groups ? (groups - gwarp + nwarps - 1) / nwarps : 0;
+  for (int st = 0; st < kBulkStages - 1; ++st) {
+    if (static_cast<uint64_t>(st) < my_groups) issue(st, st);
+  }
+  float sq = 0.0f;
+  uint32_t phase = 0;  // parity bits, one per stage
+  for (uint64_t j = 0; j < my_groups; ++j) {
+    const int st = static_cast<int>(j % kBulkStages);
+    mbar_wait(my_bars + st, (phase >> st) & 1u);
+    phase ^= 1u << st;
+    const uint32_t mask = __shfl_sync(0xFFFFFFFFu, ok_mask[st], 0);
+    // loss partial: lanes read the stage (rows k with mask bit k)
+    const float4* sp = reinterpret_cast<const float4*>(my_stages + st * kBulkStageBytes);
+#pragma unroll
+    for (int q = 0; q < static_cast<int>(kBulkStageBytes / 16 / 32); ++q) {
+      const int f4 = q * 32 + static_cast<int>(lane);
+      const int row = f4 * 16 / static_cast<int>(kRowBytes);
+      if ((mask >> row) & 1u) {
+        const float4 v = sp[f4];
+        sq = __fmaf_rn(v.x, v.x, sq);
+        sq = __fmaf_rn(v.y, v.y, sq);
+        sq = __fmaf_rn(v.z, v.z, sq);
+        sq = __fmaf_rn(v.w, v.w, sq);
+      }
+    }
+    const uint64_t gi = gwarp + j * nwarps;
+    const uint64_t row0 = gi * R;
+    if (lane == 0) {
+      const uint64_t left = occ - row0;
+      const uint32_t nrows = left < static_cast<uint64_t>(R) ? static_cast<uint32_t>(left) : static_cast<uint32_t>(R);
+      const uint32_t full = nrows >= 32 ? 0xFFFFFFFFu : ((1u << nrows) - 1u);
+      if (mask == full) {  // consecutive rows of out: one store for the stage
+        bulk_store(out + row0 * DIM, my_stages + st * kBulkStageBytes, nrows * kRowBytes);
+      } else {
+        for (uint32_t m = mask; m; m &= m - 1) {
+          const int k = __ffs(m) - 1;
+          bulk_store(out + (row0 + k) * DIM, my_stages + st * kBulkStageBytes + k * kRowBytes, kRowBytes);
+        }
+      }
+      bulk_commit();
+      // the previous stage's store has read its shared memory: refill it
+      bulk_wait_read<1>();
+    }
+    __syncwarp();
+    const uint64_t jn = j + kBulkStages - 1;
+    if (jn < my_groups) issue(jn, static_cast<int>(jn % kBulkStages));
+  }
+  if (lane == 0) bulk_wait_all();
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, m);
+  if (lane == 0) s_sq[warp] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) acc += static_cast<double>(s_sq[w]);
+    loss_partials[blockIdx.x] = acc;
+  }
+}
+
 // Fixed-shape tree over the partials (thread t sums t, t+1024, ... in order,
 // then a fixed shared-memory tree): deterministic for a fixed grid.
 __global__ void __launch_bounds__(1024)
@@ -813,9 +970,27 @@ void set_compute_blocks_per_sm(unsigned per_sm) { g_compute_blocks_per_sm = per_
 
 void launch_gather_local(const uint32_t* rows, uint64_t occ, const float* weights, float* out,
                          const RemapView& remap, uint32_t dim, double* loss_partials,
-                         unsigned grid, cudaStream_t stream) {
+                         unsigned grid, cudaStream_t stream, int bulk_stages) {
   dispatch_dim(dim, [&](auto D) {
     constexpr int DIM = decltype(D)::value;
+    if (bulk_stages > 0) {
+      // grid = blocks per SM x SMs, each block 4 warps with bulk_stages
+      // stages of 4 KB each
+      const int stages = std::min(kBulkMaxStages, std::max(2, bulk_stages));
+      const size_t smem = 8 * (kBulkThreads / 32) * kBulkMaxStages +
+                          static_cast<size_t>(kBulkThreads / 32) * stages * kBulkStageBytes;
+      static const bool attr = [] {  // the largest ring, once per instantiation
+        const size_t most = 8 * (kBulkThreads / 32) * kBulkMaxStages +
+                            static_cast<size_t>(kBulkThreads / 32) * kBulkMaxStages * kBulkStageBytes;
+        TSD_CUDA(cudaFuncSetAttribute(gather_bulk_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(most)));
+        return true;
+      }();
+      (void)attr;
+      gather_bulk_kernel<DIM><<<grid, kBulkThreads, smem, stream>>>(rows, occ, weights, out, remap,
+                                                                     loss_partials, stages);
+      return;
+    }
     constexpr int UNROLL = DIM <= 128 ? 8 : (DIM <= 256 ? 4 : 2);
     gather_local_kernel<DIM, UNROLL><<<grid, kThreads, 0, stream>>>(rows, occ, weights, out, remap,
                                                                      loss_partials);

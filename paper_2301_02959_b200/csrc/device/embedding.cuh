@@ -66,9 +66,11 @@ struct GradSource {
 // out[i] = W[local(rows[i])] for every occurrence served locally; remote
 // occurrences are skipped (filled by the exchange).  Writes per-block
 // partial sums of out^2 (double) into loss_partials[gridDim.x].
+// bulk_stages > 0: the bulk-copy variant (gather_bulk_kernel: 4-warp blocks,
+// bulk_stages x 4 KB shared-memory stages per warp), else the register one.
 void launch_gather_local(const uint32_t* rows, uint64_t occ, const float* weights, float* out,
                          const RemapView& remap, uint32_t dim, double* loss_partials,
-                         unsigned grid, cudaStream_t stream);
+                         unsigned grid, cudaStream_t stream, int bulk_stages = 0);
 unsigned gather_grid(uint64_t occ);
 // Blocks per SM of the compute-stream persistent grids (8 = whole SM; the
 // table sets 6 when U > 1 so comm-stream kernels keep two slots per SM).

@@ -181,6 +181,7 @@ struct ts_table {
   uint32_t* dd_keys = nullptr;
   uint32_t* dd_vals = nullptr;
   unsigned fwd_gather_grid = 0;
+  int gather_bulk_stages = 2;  // 0 = register gather (set at creation)
   cudaEvent_t ev_ids = nullptr, ev_fwd = nullptr, ev_bwd0 = nullptr, ev_grads = nullptr,
               ev_dense = nullptr, ev_ar = nullptr;
   ncclComm_t world = nullptr, intra = nullptr, cross = nullptr;
@@ -514,13 +515,29 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
   // ---- step buffers ----------------------------------------------------------
   gather_grid = tsd::gather_grid(c.max_occurrences);
   fwd_gather_grid = gather_grid;
+  {
+    // forward gather variant (TIERSHARD_GATHER=bulk|reg): at U = 1 the
+    // bulk-copy gather, whose rows never pass through registers, so it
+    // holds few warps and the dedup sort beside it gets the rest of each SM.
+    // Measured at C2, N=1 (step ms / gather / sort, tools/gather_ab.sh):
+    // register 6 blocks/SM 1.304 / 0.56 / 0.66; bulk 5 blocks x 2 stages
+    // 1.230 / 0.63 / 0.53; bulk 6 x 2 1.297 (gather alone 0.53 ms, the
+    // fastest); bulk 3 x 3 1.252; bulk 2 x 3 1.385 (sort 0.30, gather 0.79)
+    // -- the two kernels trade shared memory, the step follows the slower.
+    const char* ge = std::getenv("TIERSHARD_GATHER");
+    const bool bulk = ge ? std::string(ge) == "bulk" : U == 1;
+    if (const char* se = std::getenv("TIERSHARD_BULK_STAGES")) gather_bulk_stages = std::max(2, std::atoi(se));
+    if (!bulk) gather_bulk_stages = 0;
+  }
   if (aux) {
     const char* e = std::getenv("TIERSHARD_GATHER_BLOCKS");
-    // 6 blocks per SM leave the dedup sort room beside the gather (C2, N=1:
-    // 8 -> 1.318 ms/step, 6 -> 1.307, 4 -> 1.328; aux at high priority).  At
-    // U > 1 8 stays best (N=2: 2.33 ms against 2.35-2.36 with 6; a high-
-    // priority aux there costs 0.1 ms: the sort then delays serve and push)
-    const unsigned per_sm = e ? static_cast<unsigned>(std::max(1, std::atoi(e))) : (U == 1 ? 6u : 8u);
+    // register gather: 6 blocks per SM leave the dedup sort room beside the
+    // gather (C2, N=1: 8 -> 1.318 ms/step, 6 -> 1.307, 4 -> 1.328; aux at
+    // high priority).  At U > 1 8 stays best (N=2: 2.33 ms against
+    // 2.35-2.36 with 6; a high-priority aux there costs 0.1 ms: the sort
+    // then delays serve and push).  Bulk gather: 5 (above).
+    const unsigned per_sm = e ? static_cast<unsigned>(std::max(1, std::atoi(e)))
+                              : (gather_bulk_stages ? 5u : (U == 1 ? 6u : 8u));
     fwd_gather_grid = std::min(gather_grid, static_cast<unsigned>(tsd::sm_count()) * per_sm);
   }
   // [local gather partials | remote partials: staged scatter (gather_grid) or
@@ -923,7 +940,8 @@ void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   if (U == 1) {
     if (aux) TSD_CUDA(cudaEventRecord(ev_fwd0, stream));  // the ids are in place
     int t = phase_begin(kPhaseGather);
-    launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, fwd_gather_grid, stream);
+    launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, fwd_gather_grid, stream,
+                        gather_bulk_stages);
     phase_end(t);
     launch_loss_finalize(loss_partials.ptr, gather_grid, d_loss.ptr, stream);
     n_local_occ = occ;
@@ -1026,7 +1044,8 @@ void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   TSD_CUDA(cudaEventRecord(ev_fwd, comm));
 
   t = phase_begin(kPhaseGather);
-  launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, gather_grid, stream);
+  launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, gather_grid, stream,
+                      gather_bulk_stages);
   phase_end(t);
   TSD_CUDA(cudaStreamWaitEvent(stream, ev_fwd, 0));
   // loss = local-gather partials + scatter partials, fixed order
@@ -1334,7 +1353,8 @@ void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   TSD_CUDA(cudaEventRecord(ev_fwd, comm));
 
   t = phase_begin(kPhaseGather);
-  launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, fwd_gather_grid, stream);
+  launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, fwd_gather_grid, stream,
+                      gather_bulk_stages);
   phase_end(t);
   TSD_CUDA(cudaStreamWaitEvent(stream, ev_fwd, 0));
   launch_loss_finalize(loss_partials.ptr, static_cast<unsigned>(gather_grid + remote_loss_slots), d_loss.ptr,
