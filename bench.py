@@ -259,7 +259,7 @@ PHASE_BYTES_DOC = {
 
 
 PHASE_KERNELS = {
-    "gather": ["gather_local_kernel"],
+    "gather": ["gather_bulk_kernel (U=1)", "gather_local_kernel (U>1)"],
     "segment_update": ["seg_short_kernel", "long_prefix_kernel", "piece_kernel", "long_combine_kernel"],
     "dedup_sort": ["onesweep_hist_kernel", "onesweep_offsets_kernel", "onesweep_pass_kernel"],
 }
@@ -643,6 +643,10 @@ def run_ours(args, dist: Dist):
                 "achieved": round(achieved, 1),
                 "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
                 "traffic": traffic, "traffic_source": traffic_src,
+                # DRAM bytes the kernels really moved per step (ncu) over the
+                # same in-step time: below `frac` where L2 hits serve reads
+                "traffic_frac": (round(traffic / (per_launch_ms[dominant] / 1e3) / 1e9 / hbm_peak, 4)
+                                 if traffic else None),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
                 "algorithmic_bytes_per_step": algo[dominant], "avg_step_ms": per_launch_ms[dominant],
                 "bytes_model": PHASE_BYTES_DOC[dominant],
