@@ -135,4 +135,18 @@ void launch_push_grads(const PushTable& t, const uint32_t* order, const float* g
 void launch_serve_rows(const float* weights, const uint32_t* recv_ids, const uint32_t* recv_pos,
                        const ServeTable& st, uint32_t dim, cudaStream_t stream);
 
+// Device-side rendezvous over peer memory (one process per GPU): rank `me`
+// stores `value` into slot [me] of every peer's flag mailbox (release,
+// system scope) and one warp spins until every peer has stored it into its
+// own mailbox (acquire).  Work queued before it on the stream, on every
+// rank, completes before work queued after it -- the ordering of the NCCL
+// 1-int all-reduce it replaces, with one 32-thread block instead of NCCL's
+// grid and no host involvement.  `value` increases by one per rendezvous.
+struct FlagBarrier {
+  uint64_t* peer_flags[kMaxPeerRanks];  // each rank's mailbox (ours at [me])
+  int n;
+  int me;
+};
+void launch_flag_barrier(const FlagBarrier& b, uint64_t value, cudaStream_t stream);
+
 }  // namespace tsd

@@ -243,6 +243,12 @@ struct ts_table {
   tsd::DevBuf<uint32_t> recv_pos;
   tsd::DevBuf<uint8_t> xfer;  // all-gather scratch [U x bytes]
   tsd::DevBuf<int32_t> barrier_buf;
+  // peer-memory flag rendezvous (one process per GPU; TIERSHARD_BARRIER=nccl
+  // keeps the NCCL all-reduce): mailbox of U u64 flags, exported at setup
+  tsd::DevBuf<uint64_t> flag_box;
+  tsd::FlagBarrier flag_barrier{};
+  bool flag_barriers = false;
+  uint64_t barrier_seq = 0;
   std::vector<uint8_t> h_xfer;
   std::vector<const uint32_t*> peer_ids, peer_pos;  // peers' request lists (mapped)
   std::vector<double*> peer_loss;                   // peers' remote-loss slots (mapped)
@@ -633,6 +639,10 @@ void ts_table::barrier_on_comm() {
     group_barrier(grp, g, comm);
     return;
   }
+  if (flag_barriers) {
+    launch_flag_barrier(flag_barrier, ++barrier_seq, comm);
+    return;
+  }
   TSD_NCCL(ncclAllReduce(barrier_buf.ptr, barrier_buf.ptr, 1, ncclInt32, ncclSum, world, comm));
 }
 
@@ -705,12 +715,15 @@ void ts_table::setup_p2p() {
     std::memset(&e, 0, sizeof(e));
     return p ? (grp ? direct_export(p) : export_pointer(p)) : e;
   };
-  constexpr int kExports = 10;
+  flag_box.ensure(kMaxPeerRanks);
+  TSD_CUDA(cudaMemsetAsync(flag_box.ptr, 0, sizeof(uint64_t) * kMaxPeerRanks, comm));
+  TSD_CUDA(cudaStreamSynchronize(comm));
+  constexpr int kExports = 11;
   IpcExport mine[kExports] = {export_ptr(send_ids.ptr), export_ptr(order.ptr),
                               export_ptr(loss_partials.ptr + gather_grid), exp_or_none(dense_dp.ptr),
                               export_ptr(d_w), exp_or_none(d_state), exp_or_none(dense_flex.ptr),
                               exp_or_none(stamp_dp.ptr), exp_or_none(stamp_flex.ptr),
-                              export_ptr(recv_rows.ptr)};
+                              export_ptr(recv_rows.ptr), export_ptr(flag_box.ptr)};
   const std::vector<uint8_t> all = allgather_bytes(mine, sizeof(mine));
   peer_ids.assign(U, nullptr);
   peer_pos.assign(U, nullptr);
@@ -742,6 +755,14 @@ void ts_table::setup_p2p() {
     peer_stamp_dp[p] = static_cast<uint32_t*>(open_opt(e[7]));
     peer_stamp_flex[p] = static_cast<uint32_t*>(open_opt(e[8]));
     peer_recv_rows[p] = static_cast<float*>(peers.open(pp, e[9]));
+    flag_barrier.peer_flags[p] = static_cast<uint64_t*>(peers.open(pp, e[10]));
+  }
+  flag_barrier.peer_flags[g] = flag_box.ptr;
+  flag_barrier.n = static_cast<int>(U);
+  flag_barrier.me = static_cast<int>(g);
+  if (!grp) {  // in-process ranks may share a GPU: a spinning block could starve a peer
+    const char* be = std::getenv("TIERSHARD_BARRIER");
+    flag_barriers = !(be && std::string(be) == "nccl");
   }
   exchange_recv_exports();
   peer_grad.assign(U, nullptr);
@@ -1647,6 +1668,7 @@ void ts_table::destroy() {
     b->release();
   }
   for (auto* b : {&partials, &send_rows, &recv_rows, &dense_dp, &dense_flex, &ar_tmp}) b->release();
+  flag_box.release();
   stamp_dp.release();
   stamp_flex.release();
   for (auto& [a, b] : ev_pool) {
