@@ -159,7 +159,23 @@ __global__ void flag_barrier_kernel(FlagBarrier b, uint64_t value) {
   __threadfence_system();
 }
 
+__global__ void mailbox_put_kernel(MailboxPut m, const uint32_t* __restrict__ src, uint32_t words, size_t offset) {
+  for (int p = 0; p < m.n; ++p) {
+    if (p == m.me) continue;
+    uint32_t* dst = reinterpret_cast<uint32_t*>(m.peer_box[p] + offset);
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+  }
+  __threadfence_system();
+}
+
 }  // namespace
+
+void launch_mailbox_put(const MailboxPut& m, const uint8_t* src, size_t bytes, size_t offset,
+                        cudaStream_t stream) {
+  mailbox_put_kernel<<<1, 128, 0, stream>>>(m, reinterpret_cast<const uint32_t*>(src),
+                                           static_cast<uint32_t>(bytes / 4), offset);
+  TSD_LAUNCH_CHECK();
+}
 
 void launch_flag_barrier(const FlagBarrier& b, uint64_t value, cudaStream_t stream) {
   flag_barrier_kernel<<<1, 32, 0, stream>>>(b, value);

@@ -149,4 +149,15 @@ struct FlagBarrier {
 };
 void launch_flag_barrier(const FlagBarrier& b, uint64_t value, cudaStream_t stream);
 
+// All-gather through peer mailboxes: `bytes` (a multiple of 4) from `src`
+// are stored at offset `offset` of every other rank's mailbox (one block;
+// the flag rendezvous that follows publishes them).
+struct MailboxPut {
+  uint8_t* peer_box[kMaxPeerRanks];
+  int n;
+  int me;
+};
+void launch_mailbox_put(const MailboxPut& m, const uint8_t* src, size_t bytes, size_t offset,
+                        cudaStream_t stream);
+
 }  // namespace tsd

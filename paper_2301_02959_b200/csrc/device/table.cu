@@ -247,7 +247,19 @@ struct ts_table {
   // keeps the NCCL all-reduce): mailbox of U u64 flags, exported at setup
   tsd::DevBuf<uint64_t> flag_box;
   tsd::FlagBarrier flag_barrier{};
+  // per-step payload mailbox [U x step_payload_bytes] (flag mode): every
+  // rank's bucket starts + output export, stored by the ranks themselves
+  tsd::DevBuf<uint8_t> mbox;
+  tsd::MailboxPut mbox_put{};
   bool flag_barriers = false;
+  // TIERSHARD_FWD_COUNTS=mailbox: the forward's count exchange through the
+  // mailboxes + a flag rendezvous, with the local gather queued before it;
+  // default: the NCCL all-gather, gather after.  Measured at C2 (ms/step,
+  // tools/mg_env_ab.sh): N=2 2.29 (all-gather) vs 2.32-2.45 (mailbox, 6-8
+  // gather blocks/SM); N=4 3.27 vs 3.34 -- the early gather takes the SMs
+  // the serve and the sort then wait for; the step is bound by the sum of
+  // concurrent HBM + NVLink work, not by the exchange's latency.
+  bool mailbox_counts = false;
   uint64_t barrier_seq = 0;
   std::vector<uint8_t> h_xfer;
   std::vector<const uint32_t*> peer_ids, peer_pos;  // peers' request lists (mapped)
@@ -717,13 +729,14 @@ void ts_table::setup_p2p() {
   };
   flag_box.ensure(kMaxPeerRanks);
   TSD_CUDA(cudaMemsetAsync(flag_box.ptr, 0, sizeof(uint64_t) * kMaxPeerRanks, comm));
+  mbox.ensure(step_payload_bytes() * U);
   TSD_CUDA(cudaStreamSynchronize(comm));
-  constexpr int kExports = 11;
+  constexpr int kExports = 12;
   IpcExport mine[kExports] = {export_ptr(send_ids.ptr), export_ptr(order.ptr),
                               export_ptr(loss_partials.ptr + gather_grid), exp_or_none(dense_dp.ptr),
                               export_ptr(d_w), exp_or_none(d_state), exp_or_none(dense_flex.ptr),
                               exp_or_none(stamp_dp.ptr), exp_or_none(stamp_flex.ptr),
-                              export_ptr(recv_rows.ptr), export_ptr(flag_box.ptr)};
+                              export_ptr(recv_rows.ptr), export_ptr(flag_box.ptr), export_ptr(mbox.ptr)};
   const std::vector<uint8_t> all = allgather_bytes(mine, sizeof(mine));
   peer_ids.assign(U, nullptr);
   peer_pos.assign(U, nullptr);
@@ -756,13 +769,19 @@ void ts_table::setup_p2p() {
     peer_stamp_flex[p] = static_cast<uint32_t*>(open_opt(e[8]));
     peer_recv_rows[p] = static_cast<float*>(peers.open(pp, e[9]));
     flag_barrier.peer_flags[p] = static_cast<uint64_t*>(peers.open(pp, e[10]));
+    mbox_put.peer_box[p] = static_cast<uint8_t*>(peers.open(pp, e[11]));
   }
+  mbox_put.peer_box[g] = mbox.ptr;
+  mbox_put.n = static_cast<int>(U);
+  mbox_put.me = static_cast<int>(g);
   flag_barrier.peer_flags[g] = flag_box.ptr;
   flag_barrier.n = static_cast<int>(U);
   flag_barrier.me = static_cast<int>(g);
   if (!grp) {  // in-process ranks may share a GPU: a spinning block could starve a peer
     const char* be = std::getenv("TIERSHARD_BARRIER");
     flag_barriers = !(be && std::string(be) == "nccl");
+    const char* ce = std::getenv("TIERSHARD_FWD_COUNTS");
+    mailbox_counts = flag_barriers && ce && std::string(ce) == "mailbox";
   }
   exchange_recv_exports();
   peer_grad.assign(U, nullptr);
@@ -1255,7 +1274,10 @@ void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   const RemapView rv = remap_view();
   const size_t P = step_payload_bytes();
   const size_t starts_bytes = P - sizeof(IpcExport);
-  uint8_t* my_slot = xfer.ptr + P * g;
+  // mailbox mode: the payload goes through the peers' mailboxes, so the
+  // local gather is queued before the exchange of counts (no NCCL kernel
+  // for it to starve of SMs) and runs while the host waits for them
+  uint8_t* my_slot = (mailbox_counts ? mbox.ptr : xfer.ptr) + P * g;
 
   // ---- route: bucket + one stable counting pass; request lists in HBM -----
   int t = phase_begin(kPhaseRoute);
@@ -1288,7 +1310,16 @@ void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   TSD_CUDA(cudaEventRecord(ev_ids, stream));
   TSD_CUDA(cudaStreamWaitEvent(comm, ev_ids, 0));
   h_xfer.resize(P * U);
-  if (grp) {
+  if (mailbox_counts) {
+    t = phase_begin(kPhaseGather);
+    launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, fwd_gather_grid, stream,
+                        gather_bulk_stages);
+    phase_end(t);
+    launch_mailbox_put(mbox_put, my_slot, P, P * g, comm);
+    barrier_on_comm();
+    TSD_CUDA(cudaMemcpyAsync(h_xfer.data(), mbox.ptr, P * U, cudaMemcpyDeviceToHost, comm));
+    TSD_CUDA(cudaStreamSynchronize(comm));
+  } else if (grp) {
     // in-process: this rank's slot to the host, then a host all-gather.
     // Every rank synchronised its comm stream (which waited for the route)
     // before the gather, so the request lists are complete before any pull
@@ -1373,10 +1404,12 @@ void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   phase_end(t);
   TSD_CUDA(cudaEventRecord(ev_fwd, comm));
 
-  t = phase_begin(kPhaseGather);
-  launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, fwd_gather_grid, stream,
-                      gather_bulk_stages);
-  phase_end(t);
+  if (!mailbox_counts) {
+    t = phase_begin(kPhaseGather);
+    launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, fwd_gather_grid, stream,
+                        gather_bulk_stages);
+    phase_end(t);
+  }
   TSD_CUDA(cudaStreamWaitEvent(stream, ev_fwd, 0));
   launch_loss_finalize(loss_partials.ptr, static_cast<unsigned>(gather_grid + remote_loss_slots), d_loss.ptr,
                        stream);
@@ -1669,6 +1702,7 @@ void ts_table::destroy() {
   }
   for (auto* b : {&partials, &send_rows, &recv_rows, &dense_dp, &dense_flex, &ar_tmp}) b->release();
   flag_box.release();
+  mbox.release();
   stamp_dp.release();
   stamp_flex.release();
   for (auto& [a, b] : ev_pool) {
