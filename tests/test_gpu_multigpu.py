@@ -73,7 +73,7 @@ CASES = [(1, 2, 1, "p2p"), (2, 1, 1, "p2p"), (2, 1, 0, "p2p"), (2, 2, 1, "p2p"),
          (1, 2, 1, "p2p_pull"), (2, 2, 1, "p2p_pull"), (1, 4, 0, "p2p_pull"),
          (1, 2, 1, "nccl"), (2, 2, 1, "nccl"), (2, 1, 0, "nccl"),
          (1, 2, 1, "p2p_short8"), (2, 2, 1, "p2p_short8"), (1, 2, 1, "p2p_serial"),
-         (1, 2, 1, "p2p_regrow"), (2, 2, 0, "p2p_regrow")]
+         (1, 2, 1, "p2p_regrow"), (2, 2, 0, "p2p_regrow"), (1, 2, 1, "p2p_mailbox"), (2, 2, 1, "p2p_mailbox")]
 # always in-process (ts_group): the C2 topologies at logical U = 8 on however
 # many GPUs the box has (several ranks per GPU), and a 2-per-GPU mix
 INPROC_CASES = [(1, 8, 1, "p2p"), (2, 4, 1, "p2p"), (2, 4, 0, "nccl"), (1, 3, 1, "p2p"), (3, 2, 1, "p2p_pull")]
@@ -85,6 +85,8 @@ def case_env(exchange):
                TIERSHARD_LONG_CONCURRENT="0" if exchange == "p2p_serial" else "1")
     if exchange == "p2p_short8":
         env["TIERSHARD_SHORT_MAX"] = "8"
+    if exchange == "p2p_mailbox":
+        env["TIERSHARD_FWD_COUNTS"] = "mailbox"
     return env
 
 
@@ -175,7 +177,9 @@ def test_multi_gpu_matches_oracle(cuda, tmp_path, n_nodes, w, opt, exchange):
     piece path on the aux stream (TIERSHARD_SHORT_MAX=8), "p2p_serial" = long
     segments after the short kernel (TIERSHARD_LONG_CONCURRENT=0),
     "p2p_regrow" = a 16-row gradient receive buffer (recv_rows_hint): the
-    step takes the collective regrowth path first."""
+    step takes the collective regrowth path first, "p2p_mailbox" = counts
+    through the peer mailboxes (TIERSHARD_FWD_COUNTS=mailbox; one process
+    per GPU only -- the in-process group keeps its host all-gather)."""
     res = run_case(tmp_path, n_nodes, w, opt, lr_for(n_nodes * w), exchange)
     check_one_step(res, n_nodes, w, opt, lr_for(n_nodes * w))
     if exchange == "p2p_regrow":  # the path was taken, collectively
