@@ -43,6 +43,7 @@ def run(alpha, nodes, w, goal, bw, rows, tmp):
         "saved_vs_rw_GB": (off["rw_bytes"] - plan_off) / 1e9,
         "saved_vs_tw_GB": (off["tw_bytes"] - plan_off) / 1e9,
         "max_send_GB": {k: v / 1e9 for k, v in tr["max_send_bytes"].items()},
+        "max_send_off_device_GB": {k: v / 1e9 for k, v in tr["max_send_off_device_bytes"].items()},
     }
 
 
@@ -61,7 +62,8 @@ def main():
                 print(f"alpha={alpha:4} {r['topology']} {goal}: dp={r['dp_cut']} flex={r['flex_cut'] - r['dp_cut']} "
                       f"reduction pred={r['predicted_global_a2a_reduction']:.4f} "
                       f"meas={r['measured_global_a2a_reduction']:.4f} off-device GB plan/rw/tw = "
-                      f"{r['off_device_GB']['plan']:.3f}/{r['off_device_GB']['rw']:.3f}/{r['off_device_GB']['tw']:.3f}",
+                      f"{r['off_device_GB']['plan']:.3f}/{r['off_device_GB']['rw']:.3f}/{r['off_device_GB']['tw']:.3f} "
+                      f"max-send off-device GB plan/rw/tw = " + "/".join(f"{r['max_send_off_device_GB'][k]:.3f}" for k in ("plan", "rw", "tw")),
                       flush=True)
     Path(args.out).write_text(json.dumps(dict(
         description=__doc__.strip().splitlines()[0], rows_per_table=args.rows, results=res), indent=1) + "\n")
