@@ -128,7 +128,7 @@ typedef struct ts_keymap ts_keymap;
 
 /* Uploads the canonical order: row i of the plan is (table_ids[i],
  * row_ids[i]).  ValidationError on duplicate keys; ConfigError when table
- * ids reach 2^24 or row ids are too sparse for the dense map. */
+ * ids reach 2^24, row ids reach 2^40 or are too sparse for the dense map. */
 ts_status ts_keymap_create(ts_keymap** out, int device, uint64_t n_rows,
                            const uint32_t* table_ids, const uint64_t* row_ids);
 
@@ -374,10 +374,11 @@ ts_status ts_table_phase_trace(ts_table* t, int* phase, int* stream_id, double* 
                                double* t1_ms, int capacity, int* count);
 
 /* ts_table_forward with raw (table_id, row_id) keys (ts_keymap above): the
- * lookup runs on the table's stream into the map's scratch (valid until the
- * next call, so the following ts_table_backward sees the same ids), then the
- * forward.  Synchronises once to reject absent keys (ValidationError) before
- * any row is read. */
+ * lookup runs on the table's stream into a scratch the map keeps per table
+ * (valid until that table's next call, so the following ts_table_backward
+ * sees the same ids; several tables may share one map), then the forward.
+ * Synchronises once to reject absent keys (ValidationError) before any row
+ * is read. */
 ts_status ts_table_forward_keys(ts_table* t, ts_keymap* m, const uint32_t* d_table_ids,
                                 const uint64_t* d_row_ids, uint64_t occurrences, float* d_out);
 

@@ -14,6 +14,8 @@
 // HBM-bound.  Absent keys map to kAbsent and are counted.
 #include <cuda_runtime.h>
 
+#include <map>
+
 #include <algorithm>
 #include <memory>
 #include <string>
@@ -79,13 +81,20 @@ struct ts_keymap {
   uint32_t* d_slots = nullptr;
   unsigned long long* d_count = nullptr;
   cudaStream_t stream = nullptr;
-  uint32_t* d_canon = nullptr;  // ts_table_forward_keys scratch (kept until the next call)
-  uint64_t canon_cap = 0;
+  // ts_table_forward_keys scratch, one per table: the table's backward reads
+  // its forward's ids again, so a second table sharing this map must not
+  // overwrite them (kept until that table's next call or the map's destroy)
+  struct Canon {
+    uint32_t* ptr = nullptr;
+    uint64_t cap = 0;
+  };
+  std::map<const ts_table*, Canon> canon;
 
   void destroy() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
-    cudaFree(d_canon);
+    for (auto& kv : canon) cudaFree(kv.second.ptr);
+    canon.clear();
     cudaFree(d_dir);
     cudaFree(d_slots);
     cudaFree(d_count);
@@ -110,7 +119,15 @@ ts_status ts_keymap_create(ts_keymap** out, int device, uint64_t n_rows, const u
     }
     const uint32_t n_dir = n_rows ? max_t + 1 : 0;
     std::vector<uint64_t> span(n_dir, 0);
-    for (uint64_t i = 0; i < n_rows; ++i) span[table_ids[i]] = std::max(span[table_ids[i]], row_ids[i] + 1);
+    // row ids far beyond the dense map's reach are rejected here (row_id + 1
+    // must not wrap, and the span check below needs the true extent)
+    constexpr uint64_t kMaxRowId = uint64_t{1} << 40;
+    for (uint64_t i = 0; i < n_rows; ++i) {
+      if (row_ids[i] >= kMaxRowId) {
+        fail(TS_ERR_CONFIG, "keymap: row id " + std::to_string(row_ids[i]) + " too large for the dense map (< 2^40)");
+      }
+      span[table_ids[i]] = std::max(span[table_ids[i]], row_ids[i] + 1);
+    }
     std::vector<TableDir> dir(n_dir);
     uint64_t total = 0;
     for (uint32_t t = 0; t < n_dir; ++t) {
@@ -189,6 +206,7 @@ ts_status ts_keymap_lookup(ts_keymap* m, const uint32_t* d_table_ids, const uint
 
 ts_status ts_table_forward_keys(ts_table* t, ts_keymap* m, const uint32_t* d_table_ids,
                                 const uint64_t* d_row_ids, uint64_t occ, float* d_out) {
+  uint32_t* canon_out = nullptr;
   const ts_status st = tsd::guarded([&] {
     using namespace tsd;
     if (!t || !m) fail(TS_ERR_CONFIG, "ts_table_forward_keys: null argument");
@@ -196,17 +214,19 @@ ts_status ts_table_forward_keys(ts_table* t, ts_keymap* m, const uint32_t* d_tab
     const ts_status ss = ts_table_stream(t, &s);
     if (ss != TS_OK) fail(ss, ts_last_error());
     TSD_CUDA(cudaSetDevice(m->device));
-    if (occ > m->canon_cap) {
+    ts_keymap::Canon& cb = m->canon[t];
+    if (occ > cb.cap) {
       // the table reads these ids again in backward: grow only between steps
       TSD_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(s)));
-      cudaFree(m->d_canon);
-      m->d_canon = nullptr;
-      m->canon_cap = 0;
-      TSD_CUDA(dev_alloc(&m->d_canon, sizeof(uint32_t) * occ));
-      m->canon_cap = occ;
+      cudaFree(cb.ptr);
+      cb.ptr = nullptr;
+      cb.cap = 0;
+      TSD_CUDA(dev_alloc(&cb.ptr, sizeof(uint32_t) * std::max<uint64_t>(occ, 1)));
+      cb.cap = occ;
     }
+    canon_out = cb.ptr;
     uint64_t misses = 0;
-    const ts_status ls = ts_keymap_lookup(m, d_table_ids, d_row_ids, occ, m->d_canon, s, &misses);
+    const ts_status ls = ts_keymap_lookup(m, d_table_ids, d_row_ids, occ, cb.ptr, s, &misses);
     if (ls != TS_OK) fail(ls, ts_last_error());
     if (misses) {
       fail(TS_ERR_VALIDATION, "forward_keys: " + std::to_string(misses) +
@@ -214,7 +234,7 @@ ts_status ts_table_forward_keys(ts_table* t, ts_keymap* m, const uint32_t* d_tab
     }
   });
   if (st != TS_OK) return st;
-  return ts_table_forward(t, m->d_canon, occ, d_out);
+  return ts_table_forward(t, canon_out, occ, d_out);
 }
 
 ts_status ts_keymap_destroy(ts_keymap* m) {

@@ -557,6 +557,10 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     const unsigned per_sm = e ? static_cast<unsigned>(std::max(1, std::atoi(e)))
                               : (gather_bulk_stages ? 5u : (U == 1 ? 6u : 8u));
     fwd_gather_grid = std::min(gather_grid, static_cast<unsigned>(tsd::sm_count()) * per_sm);
+    // TIERSHARD_GATHER_GRID: total blocks (fractional blocks per SM, A/B)
+    if (const char* ge2 = std::getenv("TIERSHARD_GATHER_GRID")) {
+      fwd_gather_grid = std::min(gather_grid, static_cast<unsigned>(std::max(1, std::atoi(ge2))));
+    }
   }
   // [local gather partials | remote partials: staged scatter (gather_grid) or
   //  peer servers' slots (U x kServeGrid)]; zeroed once — slots a server

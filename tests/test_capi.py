@@ -60,6 +60,14 @@ def test_group_host_side():
         assert e.value.kind == "ConfigError"
 
 
+def test_keymap_rejects_huge_row_ids_before_device():
+    """row_id + 1 must not wrap the dense map's span: rejected on
+    the host, before any device work."""
+    with pytest.raises(ts.TSError) as e:
+        ts.KeyMap(np.array([0, 0], np.uint32), np.array([5, 2**64 - 1], np.uint64))
+    assert e.value.kind == "ConfigError" and "too large" in e.value.message
+
+
 def test_config_errors_before_device():
     with pytest.raises(ts.TSError) as e:
         ts.Router(10, 5, 2, np.zeros(10, np.uint8), 1, 1)

@@ -210,6 +210,45 @@ def test_forward_keys_equals_canonical_forward(cuda, tmp_path, opt):
 
 
 @pytest.mark.gpu
+def test_forward_keys_two_tables_share_a_keymap(cuda, tmp_path):
+    """Two tables, one key map, interleaved: forward_keys(A), forward_keys(B),
+    backward(A), backward(B).  Each table's backward must see its own ids
+    (the map keeps one canonical-id scratch per table)."""
+    import torch
+    import paper_2301_02959_b200 as ts
+    art = artifacts(tmp_path, "mixed_3tier")
+    code, err = run_import(art / "plan.json", art / "assignment.csv", tmp_path / "imp")
+    assert code == 0, err
+    s, t, r, _ = load_import(tmp_path / "imp")
+    n, dim = int(s["rows"]), 32
+    rng = np.random.default_rng(8)
+    batches = [rng.integers(0, n, 9000).astype(np.uint32), rng.integers(0, n, 7000).astype(np.uint32)]
+    km = ts.KeyMap(t, r)
+    tabs, outs, keep = [], [], []
+    for k, rows in enumerate(batches):
+        tab = ts.Table(n_rows=n, dim=dim, dp_cut=s["dp_cut"], flex_cut=s["flex_cut"], optimizer=1, lr=0.05,
+                       max_occurrences=rows.size, weight_seed=20 + k)
+        out = torch.empty((rows.size, dim), dtype=torch.float32, device="cuda")
+        d_t = torch.from_numpy(t[rows].view(np.int32)).cuda()
+        d_r = torch.from_numpy(r[rows].view(np.int64)).cuda()
+        tab.forward_keys(km, d_t.data_ptr(), d_r.data_ptr(), rows.size, out.data_ptr())
+        tabs.append(tab)
+        outs.append(out)
+        keep += [d_t, d_r]
+    for tab, out in zip(tabs, outs):
+        tab.backward(out.data_ptr())
+    for k, (tab, rows) in enumerate(zip(tabs, batches)):
+        tab.synchronize()
+        w = tab.read_rows(np.arange(n, dtype=np.uint32))
+        w_ref = orc.init_table(20 + k, n, dim)
+        st_ref = np.zeros(n, np.float32)
+        orc.backward_update(w_ref, st_ref, rows, orc.gather(w_ref, rows), 1, 0.05, 1e-8)
+        assert np.array_equal(w.view(np.uint32), w_ref.view(np.uint32)), k
+        tab.close()
+    km.close()
+
+
+@pytest.mark.gpu
 def test_forward_keys_rejects_absent_key(cuda, tmp_path):
     import torch
     import paper_2301_02959_b200 as ts

@@ -11,7 +11,7 @@ if [ $# -eq 0 ]; then set -- "reg 6 4" "bulk 2 4" "bulk 3 4" "reg 8 4"; fi
 for v in "$@"; do
   set -- $v
   if [ "$1" = "bulk" ]; then G=bulk; else G=reg; fi
-  TIERSHARD_GATHER=$G TIERSHARD_GATHER_BLOCKS=$2 TIERSHARD_BULK_STAGES=$3 timeout 600 $B > gpurun_out/gab.json 2> gpurun_out/gab.err
+  env TIERSHARD_GATHER=$G TIERSHARD_GATHER_BLOCKS=$2 TIERSHARD_BULK_STAGES=$3 ${4:-} timeout 600 $B > gpurun_out/gab.json 2> gpurun_out/gab.err
   tail -1 gpurun_out/gab.json | python -c "import json,sys; d=json.loads(sys.stdin.readline()); r=d['roofline']; print('$1 blocks/SM=$2 stages=$3', d['ms_per_step'], 'gather', r['all_phases_ms_per_step'].get('gather'), 'gbs', r.get('gather_gbs'), 'sort', r['all_phases_ms_per_step'].get('dedup_sort'), 'fwd', d['lookup_exchange']['ms_per_forward'])" >> gpurun_out/gather_ab.txt 2>&1
 done
 cat gpurun_out/gather_ab.txt
