@@ -10,6 +10,8 @@
 // ts_router_iteration (csrc/device/router.cu); there is no CPU fallback.
 #include "tiershard/simulator.hpp"
 
+#include <mutex>
+#include <condition_variable>
 #include <algorithm>
 #include <array>
 #include <cmath>
@@ -287,38 +289,75 @@ SimReport simulate(const ShardingPlan& plan, const Workload& workload,
   const uint32_t iterations = workload.num_iterations();
   std::vector<IterationMetrics> results(iterations);
   const unsigned workers = std::max(1u, std::min(threads, iterations));
-  std::vector<IterationBatch> batches(workers);
   std::vector<uint64_t> counters(size_t{TS_NUM_COUNTERS} * u);
 
-  // Host threads materialize a wave of iterations; the device then routes
-  // them one by one.  Each iteration's result only depends on its index.
-  for (uint32_t first = 0; first < iterations; first += workers) {
-    const uint32_t wave = std::min<uint32_t>(workers, iterations - first);
-    std::vector<std::exception_ptr> errors(wave);
-    std::vector<std::thread> pool;
-    for (uint32_t i = 1; i < wave; ++i) {
-      pool.emplace_back([&, i] {
-        try {
-          workload.materialize_iteration(first + i, batches[i]);
-        } catch (...) {
-          errors[i] = std::current_exception();
+  // Pipeline: `workers` host threads materialize iterations (in index order
+  // of claim) into a ring of workers + 2 batch slots while this thread routes
+  // them on the device in iteration order, so host sampling overlaps device
+  // routing.  Iteration i uses slot i % K, which iteration i - K (routed
+  // already) has freed.  Each result depends only on its index.
+  const uint32_t K = workers + 2;
+  std::vector<IterationBatch> slots(K);
+  std::vector<uint8_t> ready(iterations, 0);
+  std::mutex mu;
+  std::condition_variable cv;
+  uint32_t next = 0, routed = 0;
+  std::exception_ptr error;
+  bool stop = false;
+  std::vector<std::thread> pool;
+  for (unsigned k = 0; k < workers; ++k) {
+    pool.emplace_back([&] {
+      for (;;) {
+        uint32_t it;
+        {
+          std::unique_lock<std::mutex> lk(mu);
+          if (stop || next >= iterations) return;
+          it = next++;
+          // slot it % K is free once iteration it - K has been routed
+          cv.wait(lk, [&] { return stop || it < routed + K; });
+          if (stop) return;
         }
-      });
+        try {
+          workload.materialize_iteration(it, slots[it % K]);
+        } catch (...) {
+          std::lock_guard<std::mutex> lk(mu);
+          if (!error) error = std::current_exception();
+          stop = true;
+          cv.notify_all();
+          return;
+        }
+        std::lock_guard<std::mutex> lk(mu);
+        ready[it] = 1;
+        cv.notify_all();
+      }
+    });
+  }
+  std::exception_ptr route_error;
+  for (uint32_t it = 0; it < iterations && !route_error; ++it) {
+    {
+      std::unique_lock<std::mutex> lk(mu);
+      cv.wait(lk, [&] { return stop || ready[it]; });
+      if (!ready[it]) break;  // a worker failed
     }
     try {
-      workload.materialize_iteration(first, batches[0]);
+      router.route(slots[it % K], counters.data());
+      results[it] = derive_metrics(counters.data(), u, cfg, topo, sp);
     } catch (...) {
-      errors[0] = std::current_exception();
+      route_error = std::current_exception();
     }
-    for (auto& t : pool) t.join();
-    for (auto& e : errors) {
-      if (e) std::rethrow_exception(e);
-    }
-    for (uint32_t i = 0; i < wave; ++i) {
-      router.route(batches[i], counters.data());
-      results[first + i] = derive_metrics(counters.data(), u, cfg, topo, sp);
-    }
+    std::lock_guard<std::mutex> lk(mu);
+    routed = it + 1;
+    if (route_error) stop = true;
+    cv.notify_all();
   }
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    stop = true;
+    cv.notify_all();
+  }
+  for (auto& t : pool) t.join();
+  if (route_error) std::rethrow_exception(route_error);
+  if (error) std::rethrow_exception(error);
 
   SimReport report;
   report.seed = workload.seed();
