@@ -49,7 +49,19 @@ def main():
             "dram_gbs": round(dram / t / 1e9, 1) if t else None,
             "nvlink_user_tx_gbs": round(tx_user / t / 1e9, 1) if t else None,
         }
-    json.dump({"source": label, "per_kernel": res}, open(out, "w"), indent=1)
+    # per step and rank, from the launches each makes per step: one gather,
+    # one short-segment launch per segment range (replicated, rest), and the
+    # long path (prefix, pieces, combine) once per range
+    per_step = {"seg_short_kernel (replicated range)": 1, "seg_short_kernel (rest)": 1, "piece_kernel": 2,
+                "long_combine_kernel": 2, "long_prefix_kernel": 2}
+    seg = tuple(per_step)
+    seg_bytes = sum(res[k]["dram_bytes"] * per_step[k] for k in seg if k in res)
+    n_steps = None
+    phases = {"gather": {"dram_bytes_per_step": res["gather_local_kernel"]["dram_bytes"]} if "gather_local_kernel" in res
+              else None,
+              "segment_update": {"dram_bytes_per_step": seg_bytes, "launches_per_step": per_step}
+              if any(k in res for k in seg) else None}
+    json.dump({"source": label, "per_kernel": res, "phases": phases}, open(out, "w"), indent=1)
     for k, v in res.items():
         print(k, v)
 
