@@ -192,3 +192,33 @@ def test_segment_schedules_bit_exact(cuda, monkeypatch, schedule):
     assert np.array_equal(got.view(np.uint32), w.view(np.uint32))
     assert np.array_equal(got_state.view(np.uint32), state.view(np.uint32))
     table.close()
+
+
+@pytest.mark.parametrize("graph", ["1", "0"])
+def test_train_steps_graph_bit_exact(cuda, monkeypatch, graph):
+    """ts_table_train_step(s)_host at U = 1 with the step captured into a CUDA
+    graph (TIERSHARD_GRAPH=1: re-captured every call and updated in place,
+    re-instantiated when the topology changes -- e.g. an empty batch) and
+    without: every step's loss and the final weights + state are the
+    oracle's sequential updates, bit for bit."""
+    import paper_2301_02959_b200 as ts
+    monkeypatch.setenv("TIERSHARD_GRAPH", graph)
+    n, dim, lr = 30_000, 128, 0.02
+    rng = np.random.default_rng(12)
+    sizes = [20_000, 23_000, 0, 17_000, 23_000]
+    batches = [zipf_rows(rng, n, s) if s else np.zeros(0, np.uint32) for s in sizes]
+    table = ts.Table(n_rows=n, dim=dim, dp_cut=200, flex_cut=200, weight_seed=SEED,
+                     optimizer=ts.OPT_ROWWISE_ADAGRAD, lr=lr, max_occurrences=max(sizes))
+    losses = list(table.train_steps_host(batches[:3])) + [table.train_step_host(b) for b in batches[3:]]
+    w = orc.init_table(SEED, n, dim)
+    st = np.zeros(n, np.float32)
+    for s, b in enumerate(batches):
+        out = orc.gather(w, b)
+        assert losses[s] == pytest.approx(orc.half_sq_sum(out), rel=1e-6, abs=1e-12), s
+        if b.size:
+            orc.backward_update(w, st, b, out, orc.OPT_ROWWISE_ADAGRAD, lr, 1e-8)
+    table.synchronize()
+    got_w, got_s = table.read_rows(np.arange(n, dtype=np.uint32), with_state=True)
+    assert np.array_equal(got_w.view(np.uint32), w.view(np.uint32))
+    assert np.array_equal(got_s.view(np.uint32), st.view(np.uint32))
+    table.close()
