@@ -5,7 +5,7 @@ Two checks, host only:
 * tools/skew_sweep.py runs from its tools/ location through bin/ts_driver on
   a scaled-down table, and the counted traffic agrees with the planner's
   prediction (the model-identity property, SPEC acceptance 4);
-* the committed full-size sweep (profiles/r01_skew_sweep.json) keeps the same
+* the committed full-size sweep (profiles/r02_skew_sweep.json) keeps the same
   properties, so the bytes-saved figures DESIGN.md quotes are self-consistent.
 """
 from __future__ import annotations
@@ -20,7 +20,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT / "tools"))
 import skew_sweep  # noqa: E402
 
-PROFILE = ROOT / "profiles" / "r01_skew_sweep.json"
+PROFILE = ROOT / "profiles" / "r02_skew_sweep.json"
 
 
 def check_row(r: dict) -> None:
@@ -37,6 +37,14 @@ def check_row(r: dict) -> None:
     assert r["saved_vs_rw_GB"] == pytest.approx(off["rw"] - off["plan"], abs=1e-9)
     assert r["saved_vs_tw_GB"] == pytest.approx(off["tw"] - off["plan"], abs=1e-9)
     assert r["dp_cut"] <= r["flex_cut"]
+    # the critical path: the most loaded server's off-device sends.  The plan
+    # never loads a server more than row-wise does, and with a hot tier it is
+    # below table-wise as well (hot rows are served on every GPU)
+    ms = r.get("max_send_off_device_GB")
+    if ms is not None:
+        assert ms["plan"] <= ms["rw"] + 1e-9, r
+        if r["flex_cut"] > 0:
+            assert ms["plan"] < ms["tw"], r
     if r["goal"] == "2tier":
         assert r["dp_cut"] == r["flex_cut"]
 
