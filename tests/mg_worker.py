@@ -17,7 +17,7 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
 
-def problem(n_nodes, w, seed=11, steps=1, varying=False):
+def problem(n_nodes, w, seed=11, steps=1, varying=False, dim=64):
     """rows[g] is rank g's first batch; steps > 1 adds steps_rows[s][g] for
     the host-API multi-step case, batches growing step to step (so any
     per-step buffer sized by the batch would have to move).  varying: ragged
@@ -25,7 +25,7 @@ def problem(n_nodes, w, seed=11, steps=1, varying=False):
     empty batches on rank 0 at step 7 and on every rank at step 11."""
     import oracle_bind as orc
     u = n_nodes * w
-    n, dim = 12000, 64
+    n = 12000
     dp_cut, flex_cut = 150, 1500 if n_nodes * w > 1 else 150
     rng = np.random.default_rng(seed)
     p = np.arange(1, n + 1, dtype=np.float64) ** -1.1
@@ -49,7 +49,8 @@ def problem(n_nodes, w, seed=11, steps=1, varying=False):
                 slot=slot, dest=dest, steps_rows=steps_rows)
 
 
-def rank_body(rank, nodes, w, optimizer, lr, steps, pipelined, device, recv_hint=0, varying=False, **table_kw):
+def rank_body(rank, nodes, w, optimizer, lr, steps, pipelined, device, recv_hint=0, varying=False, dim=64,
+              **table_kw):
     """One rank's forward + backward (steps == 1, device buffers) or `steps`
     host-buffer steps, through the C-ABI; returns what the parent test
     checks.  table_kw carries the transport: nccl_unique_id (one process per
@@ -58,7 +59,7 @@ def rank_body(rank, nodes, w, optimizer, lr, steps, pipelined, device, recv_hint
     import paper_2301_02959_b200 as ts
 
     torch.cuda.set_device(device)
-    pb = problem(nodes, w, steps=steps, varying=varying)
+    pb = problem(nodes, w, steps=steps, varying=varying, dim=dim)
     table = ts.Table(n_rows=pb["n"], dim=pb["dim"], dp_cut=pb["dp_cut"], flex_cut=pb["flex_cut"],
                      tier_dest=pb["dest"], num_nodes=nodes, gpus_per_node=w,
                      rank=rank, device=device, weight_seed=77, optimizer=optimizer, lr=lr,
@@ -95,7 +96,7 @@ def rank_body(rank, nodes, w, optimizer, lr, steps, pipelined, device, recv_hint
     return res
 
 
-def run_inproc(nodes, w, optimizer, lr, steps=1, pipelined=False, env=None, recv_hint=0, varying=False):
+def run_inproc(nodes, w, optimizer, lr, steps=1, pipelined=False, env=None, recv_hint=0, varying=False, dim=64):
     """All U ranks as threads of this process over one ts_group (rank g on
     GPU g % device_count, so several ranks share a GPU on a small box)."""
     import threading
@@ -113,7 +114,7 @@ def run_inproc(nodes, w, optimizer, lr, steps=1, pipelined=False, env=None, recv
     def body(g):
         try:
             results[g] = rank_body(g, nodes, w, optimizer, lr, steps, pipelined, g % ndev, recv_hint=recv_hint,
-                                   varying=varying, group=grp)
+                                   varying=varying, dim=dim, group=grp)
         except BaseException as e:  # noqa: BLE001 - reported by the caller
             errors[g] = e
             grp.abort()  # the other ranks' collectives fail now, not at the timeout

@@ -130,10 +130,10 @@ def assert_rows_close(got, ref, before, rtol=1e-6):
     assert not bad.any(), (int(bad.sum()), float((np.abs(got - ref) / np.maximum(scale, 1e-30)).max()))
 
 
-def check_one_step(res, n_nodes, w, opt, lr):
+def check_one_step(res, n_nodes, w, opt, lr, dim=64):
     """forward bit-exact, counters == the reference loop, updates == oracle."""
     u = n_nodes * w
-    pb = mg_worker.problem(n_nodes, w)
+    pb = mg_worker.problem(n_nodes, w, dim=dim)
     n, dim, dp, fx = pb["n"], pb["dim"], pb["dp_cut"], pb["flex_cut"]
     w0 = orc.init_table(77, n, dim)
 
@@ -227,6 +227,14 @@ def test_multi_gpu_host_steps_match_oracle(cuda, tmp_path, n_nodes, w, opt, pipe
         np.testing.assert_allclose(res[g]["weights"], w_ref[stored], rtol=1e-6, atol=1e-8)
     for g in range(1, u):
         assert np.array_equal(res[g]["weights"][:dp].view(np.uint32), res[0]["weights"][:dp].view(np.uint32))
+
+
+@pytest.mark.parametrize("dim,opt", [(512, 1), (1024, 0), (32, 1)])
+def test_inproc_wide_and_narrow_rows(cuda, dim, opt):
+    """The U > 1 kernels at the dispatch extremes (serve / push / replica
+    update templates for D = 32 .. 1024), 2 x 2 ranks in-process."""
+    res = mg_worker.run_inproc(2, 2, opt, lr_for(4), dim=dim)
+    check_one_step(res, 2, 2, opt, lr_for(4), dim=dim)
 
 
 @pytest.mark.parametrize("n_nodes,w,pipelined", [(1, 2, True), (2, 2, False)])

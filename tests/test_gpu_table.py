@@ -46,7 +46,7 @@ def run_step(table, rows, dim):
     return out, loss
 
 
-@pytest.mark.parametrize("dim", [32, 64, 128, 256])
+@pytest.mark.parametrize("dim", [32, 64, 128, 256, 512, 1024])
 @pytest.mark.parametrize("optimizer", [orc.OPT_SGD, orc.OPT_ROWWISE_ADAGRAD])
 def test_single_gpu_step_bit_exact(cuda, dim, optimizer):
     import paper_2301_02959_b200 as ts
