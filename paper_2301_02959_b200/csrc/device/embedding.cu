@@ -304,6 +304,109 @@ gather_bulk_kernel(const uint32_t* __restrict__ rows, uint64_t occ, const float*
   }
 }
 
+// Requester-pull gather (launch_gather_all): like gather_local_kernel, but
+// an occurrence served by a peer is loaded from that peer's shard over
+// NVLink instead of being skipped.
+template <int DIM, int UNROLL>
+__global__ void __launch_bounds__(kThreads)
+gather_all_kernel(const uint32_t* __restrict__ rows, uint64_t occ, PeerWeights pw, float* __restrict__ out,
+                  RemapView rv, double* __restrict__ loss_partials) {
+  constexpr int VEC = DIM / 32;
+  __shared__ float s_sq[kThreads / 32];
+  const unsigned lane = threadIdx.x & 31u;
+  const uint64_t gwarp = (static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * kThreads) >> 5;
+  float sq = 0.0f;
+  for (uint64_t base = gwarp * UNROLL; base < occ; base += nwarps * UNROLL) {
+    uint32_t my_lid = 0, my_server = rv.rank;
+    if (lane < UNROLL && base + lane < occ) {
+      const uint32_t c = __ldg(rows + base + lane);
+      if (c < rv.dp_cut) {
+        my_lid = c;
+      } else {
+        const uint32_t d = __ldg(rv.dest + c);
+        my_server = c < rv.flex_cut ? pw.node_base + d : d;
+        my_lid = __ldg(rv.local + c);
+      }
+    }
+    float r[UNROLL][VEC];
+#pragma unroll
+    for (int k = 0; k < UNROLL; ++k) {
+      const uint32_t lid = __shfl_sync(0xFFFFFFFFu, my_lid, k);
+      const uint32_t srv = __shfl_sync(0xFFFFFFFFu, my_server, k);
+      if (base + k < occ) load_lane_ro<VEC>(pw.w[srv] + static_cast<uint64_t>(lid) * DIM + lane * VEC, r[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < UNROLL; ++k) {
+      if (base + k < occ) {
+        store_lane_stream<VEC>(out + (base + k) * DIM + lane * VEC, r[k]);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) sq = __fmaf_rn(r[k][j], r[k][j], sq);
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, m);
+  if (lane == 0) s_sq[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) acc += static_cast<double>(s_sq[w]);
+    loss_partials[blockIdx.x] = acc;
+  }
+}
+
+template <int DIM, int UNROLL>
+__global__ void __launch_bounds__(kThreads)
+pull_rows_kernel(const uint32_t* __restrict__ sorted_bucket, const uint32_t* __restrict__ order,
+                 const uint32_t* __restrict__ ids, const uint32_t* __restrict__ d_count, uint64_t max_count,
+                 PeerWeights pw, uint32_t u, float* __restrict__ out, double* __restrict__ loss_partials) {
+  constexpr int VEC = DIM / 32;
+  __shared__ float s_sq[kThreads / 32];
+  const unsigned lane = threadIdx.x & 31u;
+  const uint64_t count = min(static_cast<uint64_t>(*d_count), max_count);
+  const uint64_t gwarp = (static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * kThreads) >> 5;
+  float sq = 0.0f;
+  for (uint64_t base = gwarp * UNROLL; base < count; base += nwarps * UNROLL) {
+    uint32_t my_srv = 0, my_lid = 0, my_pos = 0;
+    if (lane < UNROLL && base + lane < count) {
+      const uint64_t j = base + lane;
+      const uint32_t b = __ldg(sorted_bucket + j);
+      my_srv = b < u ? b : pw.node_base + (b - u);
+      my_lid = __ldg(ids + j);
+      my_pos = __ldg(order + j);
+    }
+    float r[UNROLL][VEC];
+#pragma unroll
+    for (int k = 0; k < UNROLL; ++k) {
+      const uint32_t srv = __shfl_sync(0xFFFFFFFFu, my_srv, k);
+      const uint32_t lid = __shfl_sync(0xFFFFFFFFu, my_lid, k);
+      if (base + k < count) load_lane_ro<VEC>(pw.w[srv] + static_cast<uint64_t>(lid) * DIM + lane * VEC, r[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < UNROLL; ++k) {
+      const uint32_t pos = __shfl_sync(0xFFFFFFFFu, my_pos, k);
+      if (base + k < count) {
+        store_lane_stream<VEC>(out + static_cast<uint64_t>(pos) * DIM + lane * VEC, r[k]);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) sq = __fmaf_rn(r[k][j], r[k][j], sq);
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, m);
+  if (lane == 0) s_sq[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) acc += static_cast<double>(s_sq[w]);
+    loss_partials[blockIdx.x] = acc;
+  }
+}
+
 // Fixed-shape tree over the partials (thread t sums t, t+1024, ... in order,
 // then a fixed shared-memory tree): deterministic for a fixed grid.
 __global__ void __launch_bounds__(1024)
@@ -994,6 +1097,30 @@ void launch_gather_local(const uint32_t* rows, uint64_t occ, const float* weight
     constexpr int UNROLL = DIM <= 128 ? 8 : (DIM <= 256 ? 4 : 2);
     gather_local_kernel<DIM, UNROLL><<<grid, kThreads, 0, stream>>>(rows, occ, weights, out, remap,
                                                                      loss_partials);
+  });
+  TSD_LAUNCH_CHECK();
+}
+
+void launch_gather_all(const uint32_t* rows, uint64_t occ, const PeerWeights& pw, float* out,
+                       const RemapView& remap, uint32_t dim, double* loss_partials, unsigned grid,
+                       cudaStream_t stream) {
+  dispatch_dim(dim, [&](auto D) {
+    constexpr int DIM = decltype(D)::value;
+    constexpr int UNROLL = DIM <= 128 ? 8 : (DIM <= 256 ? 4 : 2);
+    gather_all_kernel<DIM, UNROLL><<<grid, kThreads, 0, stream>>>(rows, occ, pw, out, remap, loss_partials);
+  });
+  TSD_LAUNCH_CHECK();
+}
+
+void launch_pull_rows(const uint32_t* sorted_bucket, const uint32_t* order, const uint32_t* ids,
+                      const uint32_t* d_count, uint64_t max_count, const PeerWeights& pw, uint32_t u,
+                      float* out, uint32_t dim, double* loss_partials, unsigned grid, cudaStream_t stream) {
+  if (max_count == 0) return;
+  dispatch_dim(dim, [&](auto D) {
+    constexpr int DIM = decltype(D)::value;
+    constexpr int UNROLL = DIM <= 128 ? 8 : (DIM <= 256 ? 4 : 2);
+    pull_rows_kernel<DIM, UNROLL><<<grid, kThreads, 0, stream>>>(sorted_bucket, order, ids, d_count, max_count,
+                                                                 pw, u, out, loss_partials);
   });
   TSD_LAUNCH_CHECK();
 }

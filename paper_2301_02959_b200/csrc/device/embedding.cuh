@@ -72,6 +72,26 @@ void launch_gather_local(const uint32_t* rows, uint64_t occ, const float* weight
                          const RemapView& remap, uint32_t dim, double* loss_partials,
                          unsigned grid, cudaStream_t stream, int bulk_stages = 0);
 unsigned gather_grid(uint64_t occ);
+
+// Requester-pull forward (U > 1, peer memory): out[i] = the row of
+// occurrence i read where it lives -- this rank's shard, or a peer's shard
+// over NVLink (weights[s] = rank s's shard, mapped; node_base = g/W*W for
+// the Flex server).  Needs no request lists and no count exchange.
+struct PeerWeights {
+  const float* w[kMaxGradPeers];
+  uint32_t node_base = 0;
+};
+void launch_gather_all(const uint32_t* rows, uint64_t occ, const PeerWeights& pw, float* out,
+                       const RemapView& remap, uint32_t dim, double* loss_partials, unsigned grid,
+                       cudaStream_t stream);
+// The remote half of the requester-pull forward: for the first *d_count
+// occurrences of the route's destination order (sorted bucket b, server
+// b < u ? b : node_base + b - u, local id ids[j], output row order[j]) load
+// the row from its server's shard over NVLink into out; per-block loss
+// partials into loss_partials[grid].
+void launch_pull_rows(const uint32_t* sorted_bucket, const uint32_t* order, const uint32_t* ids,
+                      const uint32_t* d_count, uint64_t max_count, const PeerWeights& pw, uint32_t u,
+                      float* out, uint32_t dim, double* loss_partials, unsigned grid, cudaStream_t stream);
 // Blocks per SM of the compute-stream persistent grids (8 = whole SM; the
 // table sets 6 when U > 1 so comm-stream kernels keep two slots per SM).
 void set_compute_blocks_per_sm(unsigned per_sm);

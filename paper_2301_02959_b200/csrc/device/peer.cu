@@ -139,15 +139,16 @@ pull_grads_kernel(PullGrads pg, const uint32_t* __restrict__ recv_pos, uint64_t 
   }
 }
 
-__global__ void flag_barrier_kernel(FlagBarrier b, uint64_t value) {
+__global__ void flag_barrier_kernel(FlagBarrier b, int channel, uint64_t value) {
   const int p = static_cast<int>(threadIdx.x);
+  const int off = channel * kMaxPeerRanks;
   __threadfence_system();  // this rank's earlier peer stores before its flag
   if (p < b.n && p != b.me) {
-    uint64_t* dst = b.peer_flags[p] + b.me;
+    uint64_t* dst = b.peer_flags[p] + off + b.me;
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(value) : "memory");
   }
   if (p < b.n && p != b.me) {
-    const uint64_t* src = b.peer_flags[b.me] + p;
+    const uint64_t* src = b.peer_flags[b.me] + off + p;
     uint64_t seen = 0;
     for (;;) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(seen) : "l"(src) : "memory");
@@ -177,8 +178,8 @@ void launch_mailbox_put(const MailboxPut& m, const uint8_t* src, size_t bytes, s
   TSD_LAUNCH_CHECK();
 }
 
-void launch_flag_barrier(const FlagBarrier& b, uint64_t value, cudaStream_t stream) {
-  flag_barrier_kernel<<<1, 32, 0, stream>>>(b, value);
+void launch_flag_barrier(const FlagBarrier& b, int channel, uint64_t value, cudaStream_t stream) {
+  flag_barrier_kernel<<<1, 32, 0, stream>>>(b, channel, value);
   TSD_LAUNCH_CHECK();
 }
 

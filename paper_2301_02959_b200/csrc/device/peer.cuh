@@ -142,12 +142,16 @@ void launch_serve_rows(const float* weights, const uint32_t* recv_ids, const uin
 // rank, completes before work queued after it -- the ordering of the NCCL
 // 1-int all-reduce it replaces, with one 32-thread block instead of NCCL's
 // grid and no host involvement.  `value` increases by one per rendezvous.
+// Mailboxes have kFlagChannels independent channels (one per stream that
+// runs rendezvous, so two streams' sequence numbers never interleave in one
+// slot): channel c of rank p is peer_flags[p] + c * kMaxPeerRanks.
+constexpr int kFlagChannels = 2;
 struct FlagBarrier {
   uint64_t* peer_flags[kMaxPeerRanks];  // each rank's mailbox (ours at [me])
   int n;
   int me;
 };
-void launch_flag_barrier(const FlagBarrier& b, uint64_t value, cudaStream_t stream);
+void launch_flag_barrier(const FlagBarrier& b, int channel, uint64_t value, cudaStream_t stream);
 
 // All-gather through peer mailboxes: `bytes` (a multiple of 4) from `src`
 // are stored at offset `offset` of every other rank's mailbox (one block;

@@ -260,7 +260,20 @@ struct ts_table {
   // the serve and the sort then wait for; the step is bound by the sum of
   // concurrent HBM + NVLink work, not by the exchange's latency.
   bool mailbox_counts = false;
-  uint64_t barrier_seq = 0;
+  uint64_t barrier_seq = 0, step_barrier_seq = 0;
+  // TIERSHARD_FWD=pull|serve (pull needs flag barriers or the group): the
+  // requester loads its remote rows from their owners' shards over NVLink
+  // (launch_pull_rows, on aux right after the route) instead of the owners
+  // storing them into its output after the count exchange; the counts then
+  // only feed the backward.  A rendezvous on the compute stream (channel 1)
+  // after the route makes every rank's previous update visible before any
+  // row is read.  Measured at C2, N=2 (ms/step): serve 2.28-2.32, pull
+  // 2.58-2.65 -- the random peer LOADS reach ~205 GB/s in the step (1.12 ms
+  // for 0.23 GB) where the serve's peer STORES reach ~350; a whole-batch
+  // gather with the remote loads inline (launch_gather_all) was 2.40-2.44.
+  // Kept as an option (tested), serve is the default.
+  bool pull_forward = false;
+  void forward_p2p_pull(const uint32_t* d_rows, uint64_t occ, float* d_out);
   std::vector<uint8_t> h_xfer;
   std::vector<const uint32_t*> peer_ids, peer_pos;  // peers' request lists (mapped)
   std::vector<double*> peer_loss;                   // peers' remote-loss slots (mapped)
@@ -675,7 +688,7 @@ void ts_table::barrier_on_comm() {
     return;
   }
   if (flag_barriers) {
-    launch_flag_barrier(flag_barrier, ++barrier_seq, comm);
+    launch_flag_barrier(flag_barrier, 0, ++barrier_seq, comm);
     return;
   }
   TSD_NCCL(ncclAllReduce(barrier_buf.ptr, barrier_buf.ptr, 1, ncclInt32, ncclSum, world, comm));
@@ -750,8 +763,8 @@ void ts_table::setup_p2p() {
     std::memset(&e, 0, sizeof(e));
     return p ? (grp ? direct_export(p) : export_pointer(p)) : e;
   };
-  flag_box.ensure(kMaxPeerRanks);
-  TSD_CUDA(cudaMemsetAsync(flag_box.ptr, 0, sizeof(uint64_t) * kMaxPeerRanks, comm));
+  flag_box.ensure(kFlagChannels * kMaxPeerRanks);
+  TSD_CUDA(cudaMemsetAsync(flag_box.ptr, 0, sizeof(uint64_t) * kFlagChannels * kMaxPeerRanks, comm));
   mbox.ensure(step_payload_bytes() * U);
   TSD_CUDA(cudaStreamSynchronize(comm));
   constexpr int kExports = 12;
@@ -805,6 +818,10 @@ void ts_table::setup_p2p() {
     flag_barriers = !(be && std::string(be) == "nccl");
     const char* ce = std::getenv("TIERSHARD_FWD_COUNTS");
     mailbox_counts = flag_barriers && ce && std::string(ce) == "mailbox";
+  }
+  {
+    const char* fe = std::getenv("TIERSHARD_FWD");
+    pull_forward = fe && std::string(fe) == "pull" && (flag_barriers || grp) && U <= kMaxGradPeers;
   }
   exchange_recv_exports();
   peer_grad.assign(U, nullptr);
@@ -1022,7 +1039,11 @@ void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   }
 
   if (p2p) {
-    forward_p2p(d_rows, occ, d_out);
+    if (pull_forward) {
+      forward_p2p_pull(d_rows, occ, d_out);
+    } else {
+      forward_p2p(d_rows, occ, d_out);
+    }
     return;
   }
 
@@ -1291,6 +1312,139 @@ void ts_table::backward(const float* d_grad) {
 // ---------------------------------------------------------------------------
 // peer-memory forward / backward (U > 1, one node)
 // ---------------------------------------------------------------------------
+
+void ts_table::forward_p2p_pull(const uint32_t* d_rows, uint64_t occ, float* d_out) {
+  using namespace tsd;
+  const RemapView rv = remap_view();
+  const size_t P = step_payload_bytes();
+  uint8_t* my_slot = (flag_barriers ? mbox.ptr : xfer.ptr) + P * g;
+
+  // ---- route (compute stream): request lists for the backward ------------
+  int t = phase_begin(kPhaseRoute);
+  BucketView bv;
+  bv.dest = d_dest;
+  bv.dp_cut = cfg.dp_cut;
+  bv.flex_cut = cfg.flex_cut;
+  bv.u = U;
+  bv.w = W;
+  bv.rank = g;
+  bv.slot = slot;
+  launch_bucket_keys(d_rows, occ, bv, bucket.ptr, tier_counts.ptr, stream);
+  RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, ghist.ptr, goff.ptr,
+                  sort_status.ptr, sort_counters.ptr};
+  uint32_t* sorted_b = nullptr;
+  uint32_t* sorted_i = nullptr;
+  radix_sort_pairs(bucket.ptr, nullptr, occ, bits_for(nb() - 1), rb, &sorted_b, &sorted_i, stream);
+  TSD_CUDA(cudaMemcpyAsync(order.ptr, sorted_i, sizeof(uint32_t) * occ, cudaMemcpyDeviceToDevice, stream));
+  uint32_t* my_starts = reinterpret_cast<uint32_t*>(my_slot);
+  launch_bucket_starts(goff.ptr, 1, nb(), static_cast<uint32_t>(occ), my_starts, stream);
+  launch_remote_ids_upto(d_rows, order.ptr, occ, my_starts + (U + W), d_local, send_ids.ptr, stream);
+  phase_end(t);
+  TSD_CUDA(cudaEventRecord(ev_ids, stream));
+
+  // ---- every rank's previous update done, then the rows: local ones on
+  // the compute stream, remote ones pulled over NVLink on aux -------------
+  if (grp) {
+    group_barrier(grp, g, stream);
+  } else {
+    launch_flag_barrier(flag_barrier, 1, ++step_barrier_seq, stream);
+  }
+  TSD_CUDA(cudaEventRecord(ev_fwd0, stream));  // shards final everywhere
+  PeerWeights pw;
+  for (uint32_t p = 0; p < U; ++p) pw.w[p] = peer_w[p];
+  pw.node_base = node * W;
+  t = phase_begin(kPhaseGather);
+  launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, fwd_gather_grid, stream,
+                      gather_bulk_stages);
+  phase_end(t);
+  cudaStream_t rs = aux ? aux : comm;
+  TSD_CUDA(cudaStreamWaitEvent(rs, ev_fwd0, 0));
+  t = phase_begin(kPhaseExchangeFwd, rs);
+  {
+    static const unsigned per_sm = [] {
+      const char* e = std::getenv("TIERSHARD_PULL_BLOCKS");
+      return e ? static_cast<unsigned>(std::max(1, std::atoi(e))) : 2u;
+    }();
+    const unsigned grid = static_cast<unsigned>(
+        std::min<uint64_t>(per_sm * static_cast<uint64_t>(sm_count()), remote_loss_slots));
+    launch_pull_rows(sorted_b, order.ptr, send_ids.ptr, my_starts + (U + W), occ, pw, U, d_out, cfg.dim,
+                     loss_partials.ptr + gather_grid, grid, rs);
+  }
+  phase_end(t);
+  TSD_CUDA(cudaEventRecord(ev_fwd, rs));
+  TSD_CUDA(cudaStreamWaitEvent(stream, ev_fwd, 0));
+  launch_loss_finalize(loss_partials.ptr, static_cast<unsigned>(gather_grid + remote_loss_slots), d_loss.ptr,
+                       stream);
+
+  // ---- comm stream, beside the gather: counts, then the request lists -----
+  TSD_CUDA(cudaStreamWaitEvent(comm, ev_ids, 0));
+  h_xfer.resize(P * U);
+  if (grp) {
+    std::vector<uint8_t> mine(P);
+    TSD_CUDA(cudaMemcpyAsync(mine.data(), my_slot, P, cudaMemcpyDeviceToHost, comm));
+    TSD_CUDA(cudaStreamSynchronize(comm));
+    group_allgather(grp, g, mine.data(), P, h_xfer.data());
+  } else {
+    launch_mailbox_put(mbox_put, my_slot, P, P * g, comm);
+    barrier_on_comm();
+    TSD_CUDA(cudaMemcpyAsync(h_xfer.data(), mbox.ptr, P * U, cudaMemcpyDeviceToHost, comm));
+    TSD_CUDA(cudaStreamSynchronize(comm));
+  }
+  h_counts.resize(static_cast<size_t>(U) * (nb() + 1));
+  for (uint32_t p = 0; p < U; ++p) {
+    std::memcpy(h_counts.data() + size_t{p} * (nb() + 1), h_xfer.data() + P * p, (nb() + 1) * 4);
+  }
+  ExchangePlan xp;
+  exchange_plan(N, W, g, h_counts.data(), &xp);
+  send_off = xp.send_off;
+  send_cnt = xp.send_cnt;
+  recv_off = xp.recv_off;
+  recv_cnt = xp.recv_cnt;
+  recv_before = xp.recv_before;
+  recv_total = xp.recv_total;
+  n_remote = xp.n_remote;
+  n_local_occ = occ - n_remote;
+  {
+    std::vector<uint64_t> need(U);
+    for (uint32_t p = 0; p < U; ++p) {
+      ExchangePlan pp;
+      exchange_plan(N, W, p, h_counts.data(), &pp);
+      need[p] = pp.recv_total;
+    }
+    regrow_recv(need);
+  }
+  recv_ids.ensure(recv_total);
+  recv_pos.ensure(recv_total);
+  PullTable pt{};
+  const auto start_of = [&](uint32_t p, uint32_t b) -> uint64_t { return h_counts[size_t{p} * (nb() + 1) + b]; };
+  for (uint32_t p = 0; p < U; ++p) {
+    if (p == g) continue;
+    if (recv_cnt[2 * p]) {
+      pt.seg[pt.nseg++] = PullSeg{peer_ids[p], peer_pos[p], start_of(p, g), recv_off[2 * p], recv_cnt[2 * p]};
+    }
+    if (recv_cnt[2 * p + 1]) {
+      pt.seg[pt.nseg++] = PullSeg{peer_ids[p], peer_pos[p], start_of(p, U + slot), recv_off[2 * p + 1],
+                                  recv_cnt[2 * p + 1]};
+    }
+  }
+  pt.total = recv_total;
+  if (aux) {
+    const uint64_t m = n_local_occ + recv_total;
+    entry_keys.ensure(m);
+    entry_vals.ensure(m);
+    ensure_sort_capacity(m);
+  }
+  t = phase_begin(kPhaseExchangeFwd, comm);
+  launch_pull_requests(pt, recv_ids.ptr, recv_pos.ptr, comm);
+  phase_end(t);
+  if (aux) {  // the backward's dedup needs only the ids
+    TSD_CUDA(cudaEventRecord(ev_fwd0, comm));
+    TSD_CUDA(cudaStreamWaitEvent(aux, ev_fwd0, 0));
+    dedup_p2p(aux);
+    TSD_CUDA(cudaEventRecord(ev_dedup, aux));
+    dedup_ready = true;
+  }
+}
 
 void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   using namespace tsd;

@@ -73,10 +73,12 @@ CASES = [(1, 2, 1, "p2p"), (2, 1, 1, "p2p"), (2, 1, 0, "p2p"), (2, 2, 1, "p2p"),
          (1, 2, 1, "p2p_pull"), (2, 2, 1, "p2p_pull"), (1, 4, 0, "p2p_pull"),
          (1, 2, 1, "nccl"), (2, 2, 1, "nccl"), (2, 1, 0, "nccl"),
          (1, 2, 1, "p2p_short8"), (2, 2, 1, "p2p_short8"), (1, 2, 1, "p2p_serial"),
-         (1, 2, 1, "p2p_regrow"), (2, 2, 0, "p2p_regrow"), (1, 2, 1, "p2p_mailbox"), (2, 2, 1, "p2p_mailbox")]
+         (1, 2, 1, "p2p_regrow"), (2, 2, 0, "p2p_regrow"), (1, 2, 1, "p2p_mailbox"), (2, 2, 1, "p2p_mailbox"),
+         (1, 2, 1, "p2p_fwdpull"), (2, 2, 0, "p2p_fwdpull"), (1, 4, 1, "p2p_fwdpull")]
 # always in-process (ts_group): the C2 topologies at logical U = 8 on however
 # many GPUs the box has (several ranks per GPU), and a 2-per-GPU mix
-INPROC_CASES = [(1, 8, 1, "p2p"), (2, 4, 1, "p2p"), (2, 4, 0, "nccl"), (1, 3, 1, "p2p"), (3, 2, 1, "p2p_pull")]
+INPROC_CASES = [(1, 8, 1, "p2p"), (2, 4, 1, "p2p"), (2, 4, 0, "nccl"), (1, 3, 1, "p2p"), (3, 2, 1, "p2p_pull"),
+                (2, 4, 1, "p2p_fwdpull")]
 
 
 def case_env(exchange):
@@ -87,6 +89,8 @@ def case_env(exchange):
         env["TIERSHARD_SHORT_MAX"] = "8"
     if exchange == "p2p_mailbox":
         env["TIERSHARD_FWD_COUNTS"] = "mailbox"
+    if exchange == "p2p_fwdpull":
+        env["TIERSHARD_FWD"] = "pull"
     return env
 
 
@@ -179,7 +183,8 @@ def test_multi_gpu_matches_oracle(cuda, tmp_path, n_nodes, w, opt, exchange):
     "p2p_regrow" = a 16-row gradient receive buffer (recv_rows_hint): the
     step takes the collective regrowth path first, "p2p_mailbox" = counts
     through the peer mailboxes (TIERSHARD_FWD_COUNTS=mailbox; one process
-    per GPU only -- the in-process group keeps its host all-gather)."""
+    per GPU only -- the in-process group keeps its host all-gather),
+    "p2p_fwdpull" = the requester-pull forward (TIERSHARD_FWD=pull)."""
     res = run_case(tmp_path, n_nodes, w, opt, lr_for(n_nodes * w), exchange)
     check_one_step(res, n_nodes, w, opt, lr_for(n_nodes * w))
     if exchange == "p2p_regrow":  # the path was taken, collectively
