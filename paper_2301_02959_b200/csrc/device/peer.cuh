@@ -145,7 +145,7 @@ void launch_serve_rows(const float* weights, const uint32_t* recv_ids, const uin
 // Mailboxes have kFlagChannels independent channels (one per stream that
 // runs rendezvous, so two streams' sequence numbers never interleave in one
 // slot): channel c of rank p is peer_flags[p] + c * kMaxPeerRanks.
-constexpr int kFlagChannels = 2;
+constexpr int kFlagChannels = 3;
 struct FlagBarrier {
   uint64_t* peer_flags[kMaxPeerRanks];  // each rank's mailbox (ours at [me])
   int n;

@@ -195,7 +195,10 @@ struct PassSmem {
 };
 
 template <int BINS, int kWindow>
-__global__ void __launch_bounds__(kRadixThreads, 3)
+#ifndef TSD_RADIX_MINB
+#define TSD_RADIX_MINB 3
+#endif
+__global__ void __launch_bounds__(kRadixThreads, TSD_RADIX_MINB)
 onesweep_pass_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                      uint64_t n, int shift, int bits, const uint32_t* __restrict__ goff,
                      uint64_t* __restrict__ status, uint32_t* __restrict__ tile_counter,

@@ -31,7 +31,11 @@ constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;  // 4096
 
 constexpr int kRadixThreads = 256;
-constexpr int kRadixItems = 16;
+// Items per thread of a radix tile (TSD_RADIX_ITEMS at build time, A/B).
+#ifndef TSD_RADIX_ITEMS
+#define TSD_RADIX_ITEMS 16
+#endif
+constexpr int kRadixItems = TSD_RADIX_ITEMS;
 constexpr int kRadixTile = kRadixThreads * kRadixItems;  // 4096
 constexpr int kRadixWarps = kRadixThreads / 32;
 constexpr int kRadixSubTile = kRadixTile / kRadixWarps;  // 512 items per warp

@@ -297,6 +297,23 @@ struct ts_table {
   //     their server by requester-side NVLink stores (push) or a
   //     server-side NVLink gather (pull).
   bool replica_concurrent = true;
+  // TIERSHARD_REPLICA=deferred (flag barriers or the group): the replica
+  // update runs on its own stream `rep` after the rendezvous and a second
+  // rendezvous follows it there; the step returns without waiting for it.
+  // The next forward's gather (and, with replicated Flex rows, its serve)
+  // waits for that rendezvous -- every owner's broadcast landed -- so the
+  // replica tail overlaps the next step's route, count exchange and serve.
+  // The replicated-row receive slots are double-buffered by epoch parity:
+  // step k+1's partials never land in the set step k's owners still read.
+  // Measured at C2 (ms/step, sum over steps): N=2 2.286 vs 2.290
+  // (concurrent), N=4 3.27 vs 3.28, 2x2 3.28 vs 3.32 -- the next gather
+  // needs the DP replicas (78 % of its rows), so only the route and count
+  // exchange overlap, and they compete with the broadcast.  Option, tested.
+  bool replica_deferred = false, rep_pending = false;
+  cudaStream_t rep = nullptr;
+  cudaEvent_t ev_rv = nullptr, ev_rep = nullptr;
+  uint64_t rep_barrier_seq = 0;
+  uint64_t dp_set_elems = 0, flex_set_elems = 0;  // one receive set, in floats
   bool grads_push = true;
   bool push_first = false;
 
@@ -627,13 +644,20 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     // replicated-row gradients: [U][per_dp][D] receive slots (P2P push
     // mode; the staged path uses the first dp_rows x D as a dense buffer)
     per_dp = static_cast<uint32_t>((dp_rows + U - 1) / U);
-    dense_dp.ensure(std::max<uint64_t>(uint64_t{U} * per_dp, 1) * c.dim);
-    stamp_dp.ensure(std::max<uint64_t>(uint64_t{U} * per_dp, 1));
+    {
+      const char* re = std::getenv("TIERSHARD_REPLICA");
+      replica_deferred = re && std::string(re) == "deferred";
+    }
+    const uint64_t sets = replica_deferred ? 2 : 1;
+    dp_set_elems = std::max<uint64_t>(uint64_t{U} * per_dp, 1);
+    dense_dp.ensure(sets * dp_set_elems * c.dim);
+    stamp_dp.ensure(sets * dp_set_elems);
     TSD_CUDA(cudaMemsetAsync(stamp_dp.ptr, 0, sizeof(uint32_t) * stamp_dp.cap, stream));
     if (N > 1) {
       per_flex = static_cast<uint32_t>((flex_rows + N - 1) / N);
-      dense_flex.ensure(std::max<uint64_t>(uint64_t{N} * per_flex, 1) * c.dim);
-      stamp_flex.ensure(std::max<uint64_t>(uint64_t{N} * per_flex, 1));
+      flex_set_elems = std::max<uint64_t>(uint64_t{N} * per_flex, 1);
+      dense_flex.ensure(sets * flex_set_elems * c.dim);
+      stamp_flex.ensure(sets * flex_set_elems);
       TSD_CUDA(cudaMemsetAsync(stamp_flex.ptr, 0, sizeof(uint32_t) * stamp_flex.cap, stream));
     }
     TSD_CUDA(cudaStreamSynchronize(stream));
@@ -818,6 +842,14 @@ void ts_table::setup_p2p() {
     flag_barriers = !(be && std::string(be) == "nccl");
     const char* ce = std::getenv("TIERSHARD_FWD_COUNTS");
     mailbox_counts = flag_barriers && ce && std::string(ce) == "mailbox";
+  }
+  replica_deferred = replica_deferred && (flag_barriers || grp);
+  if (replica_deferred) {
+    int lo_prio = 0, hi_prio = 0;
+    TSD_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    TSD_CUDA(cudaStreamCreateWithPriority(&rep, cudaStreamNonBlocking, hi_prio));
+    TSD_CUDA(cudaEventCreateWithFlags(&ev_rv, cudaEventDisableTiming));
+    TSD_CUDA(cudaEventCreateWithFlags(&ev_rep, cudaEventDisableTiming));
   }
   {
     const char* fe = std::getenv("TIERSHARD_FWD");
@@ -1349,6 +1381,10 @@ void ts_table::forward_p2p_pull(const uint32_t* d_rows, uint64_t occ, float* d_o
   } else {
     launch_flag_barrier(flag_barrier, 1, ++step_barrier_seq, stream);
   }
+  if (rep_pending) {
+    TSD_CUDA(cudaStreamWaitEvent(stream, ev_rep, 0));
+    rep_pending = false;
+  }
   TSD_CUDA(cudaEventRecord(ev_fwd0, stream));  // shards final everywhere
   PeerWeights pw;
   for (uint32_t p = 0; p < U; ++p) pw.w[p] = peer_w[p];
@@ -1487,6 +1523,11 @@ void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   TSD_CUDA(cudaEventRecord(ev_ids, stream));
   TSD_CUDA(cudaStreamWaitEvent(comm, ev_ids, 0));
   h_xfer.resize(P * U);
+  const bool rep_wait = rep_pending;  // the previous step's deferred replica broadcasts
+  if (rep_pending) {
+    TSD_CUDA(cudaStreamWaitEvent(stream, ev_rep, 0));
+    rep_pending = false;
+  }
   if (mailbox_counts) {
     t = phase_begin(kPhaseGather);
     launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, fwd_gather_grid, stream,
@@ -1576,6 +1617,9 @@ void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
     TSD_CUDA(cudaEventRecord(ev_dedup, aux));
     dedup_ready = true;
   }
+  // served Flex rows replicated across nodes are written by the deferred
+  // replica update: the serve waits for it (DP rows are never served)
+  if (rep_wait && N > 1 && flex_rows) TSD_CUDA(cudaStreamWaitEvent(comm, ev_rep, 0));
   launch_serve_rows(d_w, recv_ids.ptr, recv_pos.ptr, st, cfg.dim, comm);
   barrier_on_comm();  // every server has finished storing into every output
   phase_end(t);
@@ -1650,9 +1694,10 @@ void ts_table::backward_p2p(const float* d_grad) {
     d0.push_n = U;
     d0.per = per_dp;
     d0.me = g;
+    const uint64_t set = replica_deferred ? (epoch & 1u) : 0;
     for (uint32_t p = 0; p < U; ++p) {
-      d0.push_grad[p] = peer_dense_dp[p];
-      d0.push_stamp[p] = peer_stamp_dp[p];
+      d0.push_grad[p] = peer_dense_dp[p] + set * dp_set_elems * cfg.dim;
+      d0.push_stamp[p] = peer_stamp_dp[p] + set * dp_set_elems;
     }
   }
   if (N > 1 && flex_rows) {  // group: the same slot in every node, node order
@@ -1662,9 +1707,10 @@ void ts_table::backward_p2p(const float* d_grad) {
     d1.push_n = N;
     d1.per = per_flex;
     d1.me = node;
+    const uint64_t set = replica_deferred ? (epoch & 1u) : 0;
     for (uint32_t k = 0; k < N; ++k) {
-      d1.push_grad[k] = peer_dense_flex[k * W + slot];
-      d1.push_stamp[k] = peer_stamp_flex[k * W + slot];
+      d1.push_grad[k] = peer_dense_flex[k * W + slot] + set * flex_set_elems * cfg.dim;
+      d1.push_stamp[k] = peer_stamp_flex[k * W + slot] + set * flex_set_elems;
     }
   }
   // ---- remote gradient rows -> their servers -------------------------------
@@ -1773,11 +1819,16 @@ void ts_table::backward_p2p(const float* d_grad) {
   // group-rank order, updates it and broadcasts it to every replica --------
   TSD_CUDA(cudaEventRecord(ev_dense, stream));
   TSD_CUDA(cudaStreamWaitEvent(comm, ev_dense, 0));
-  cudaStream_t rs = replica_concurrent ? comm : stream;
+  cudaStream_t rs = replica_deferred ? rep : (replica_concurrent ? comm : stream);
   t = phase_begin(kPhaseRendezvous, comm);
   barrier_on_comm();
   phase_end(t);
-  if (!replica_concurrent) {
+  if (replica_deferred) {
+    TSD_CUDA(cudaEventRecord(ev_rv, comm));
+    TSD_CUDA(cudaStreamWaitEvent(rep, ev_rv, 0));
+  }
+  const uint64_t rset = replica_deferred ? (epoch & 1u) : 0;
+  if (!replica_concurrent && !replica_deferred) {
     TSD_CUDA(cudaEventRecord(ev_ar, comm));
     TSD_CUDA(cudaStreamWaitEvent(stream, ev_ar, 0));
   }
@@ -1788,8 +1839,8 @@ void ts_table::backward_p2p(const float* d_grad) {
     grp.me = static_cast<int>(g);
     grp.rows = static_cast<uint32_t>(dp_rows);
     grp.row_lo = 0;
-    grp.recv = dense_dp.ptr;
-    grp.recv_stamp = stamp_dp.ptr;
+    grp.recv = dense_dp.ptr + rset * dp_set_elems * cfg.dim;
+    grp.recv_stamp = stamp_dp.ptr + rset * dp_set_elems;
     grp.per = per_dp;
     grp.epoch = epoch;
     for (uint32_t p = 0; p < U; ++p) {
@@ -1809,14 +1860,25 @@ void ts_table::backward_p2p(const float* d_grad) {
       grp.weights[k] = peer_w[p] + dp_rows * cfg.dim;
       grp.state[k] = peer_state[p] ? peer_state[p] + dp_rows : nullptr;
     }
-    grp.recv = dense_flex.ptr;
-    grp.recv_stamp = stamp_flex.ptr;
+    grp.recv = dense_flex.ptr + rset * flex_set_elems * cfg.dim;
+    grp.recv_stamp = stamp_flex.ptr + rset * flex_set_elems;
     grp.per = per_flex;
     grp.epoch = epoch;
     launch_replica_update(grp, cfg.dim, opt, rs);
   }
   phase_end(t);
-  if (replica_concurrent) TSD_CUDA(cudaEventRecord(ev_ar, comm));
+  if (replica_deferred) {
+    // every owner's broadcast has landed everywhere once this completes
+    if (grp) {
+      group_barrier(this->grp, g, rep);
+    } else {
+      launch_flag_barrier(flag_barrier, 2, ++rep_barrier_seq, rep);
+    }
+    TSD_CUDA(cudaEventRecord(ev_rep, rep));
+    rep_pending = true;
+  } else if (replica_concurrent) {
+    TSD_CUDA(cudaEventRecord(ev_ar, comm));
+  }
   if (long_concurrent) {
     segment_range_concurrent(sk, sv, seg_split.ptr + 1, nseg.ptr, m, gs, opt, d0, d1);
   } else {
@@ -1828,7 +1890,7 @@ void ts_table::backward_p2p(const float* d_grad) {
     launch_segment_long(sk, sv, starts.ptr, m, cfg.dim, gs, d_w, d_state, opt, d0, d1, sc, stream);
     phase_end(t);
   }
-  if (replica_concurrent) TSD_CUDA(cudaStreamWaitEvent(stream, ev_ar, 0));
+  if (replica_concurrent && !replica_deferred) TSD_CUDA(cudaStreamWaitEvent(stream, ev_ar, 0));
   // peers store into our replicated rows: the next step's rendezvous (its
   // all-gather on the comm stream, after this stream's work) orders those
   // stores before any of our reads
@@ -1891,6 +1953,7 @@ void ts_table::destroy() {
   step_exec = nullptr;
   if (stream) cudaStreamSynchronize(stream);
   if (aux) cudaStreamSynchronize(aux);
+  if (rep) cudaStreamSynchronize(rep);
   if (ready && p2p) {
     // peers may still be storing into our exported buffers (replica rows,
     // gradient receive slots): a rendezvous before anything is freed
@@ -1954,6 +2017,10 @@ void ts_table::destroy() {
   rows_dev2.release();
   if (h_loss_pinned) cudaFreeHost(h_loss_pinned);
   if (comm) cudaStreamDestroy(comm);
+  if (rep) cudaStreamDestroy(rep);
+  for (cudaEvent_t e : {ev_rv, ev_rep}) {
+    if (e) cudaEventDestroy(e);
+  }
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -2252,7 +2319,7 @@ ts_status ts_table_synchronize(ts_table* t) {
       // collective: peers store into our replicated rows and receive
       // buffers, so "our step is done" means every rank's step is done --
       // a rendezvous behind all of this rank's streams, then wait for it
-      for (cudaStream_t s : {t->stream, t->aux}) {
+      for (cudaStream_t s : {t->stream, t->aux, t->rep}) {
         if (!s) continue;
         TSD_CUDA(cudaEventRecord(t->ev_ar, s));
         TSD_CUDA(cudaStreamWaitEvent(t->comm, t->ev_ar, 0));
@@ -2262,6 +2329,7 @@ ts_status ts_table_synchronize(ts_table* t) {
     TSD_CUDA(cudaStreamSynchronize(t->stream));
     if (t->aux) TSD_CUDA(cudaStreamSynchronize(t->aux));
     if (t->comm) TSD_CUDA(cudaStreamSynchronize(t->comm));
+    if (t->rep) TSD_CUDA(cudaStreamSynchronize(t->rep));
   });
 }
 

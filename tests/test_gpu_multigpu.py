@@ -74,11 +74,12 @@ CASES = [(1, 2, 1, "p2p"), (2, 1, 1, "p2p"), (2, 1, 0, "p2p"), (2, 2, 1, "p2p"),
          (1, 2, 1, "nccl"), (2, 2, 1, "nccl"), (2, 1, 0, "nccl"),
          (1, 2, 1, "p2p_short8"), (2, 2, 1, "p2p_short8"), (1, 2, 1, "p2p_serial"),
          (1, 2, 1, "p2p_regrow"), (2, 2, 0, "p2p_regrow"), (1, 2, 1, "p2p_mailbox"), (2, 2, 1, "p2p_mailbox"),
-         (1, 2, 1, "p2p_fwdpull"), (2, 2, 0, "p2p_fwdpull"), (1, 4, 1, "p2p_fwdpull")]
+         (1, 2, 1, "p2p_fwdpull"), (2, 2, 0, "p2p_fwdpull"), (1, 4, 1, "p2p_fwdpull"),
+         (1, 2, 1, "p2p_deferred"), (2, 2, 1, "p2p_deferred"), (1, 4, 0, "p2p_deferred")]
 # always in-process (ts_group): the C2 topologies at logical U = 8 on however
 # many GPUs the box has (several ranks per GPU), and a 2-per-GPU mix
 INPROC_CASES = [(1, 8, 1, "p2p"), (2, 4, 1, "p2p"), (2, 4, 0, "nccl"), (1, 3, 1, "p2p"), (3, 2, 1, "p2p_pull"),
-                (2, 4, 1, "p2p_fwdpull")]
+                (2, 4, 1, "p2p_fwdpull"), (2, 4, 1, "p2p_deferred")]
 
 
 def case_env(exchange):
@@ -91,6 +92,8 @@ def case_env(exchange):
         env["TIERSHARD_FWD_COUNTS"] = "mailbox"
     if exchange == "p2p_fwdpull":
         env["TIERSHARD_FWD"] = "pull"
+    if exchange == "p2p_deferred":
+        env["TIERSHARD_REPLICA"] = "deferred"
     return env
 
 
@@ -184,7 +187,9 @@ def test_multi_gpu_matches_oracle(cuda, tmp_path, n_nodes, w, opt, exchange):
     step takes the collective regrowth path first, "p2p_mailbox" = counts
     through the peer mailboxes (TIERSHARD_FWD_COUNTS=mailbox; one process
     per GPU only -- the in-process group keeps its host all-gather),
-    "p2p_fwdpull" = the requester-pull forward (TIERSHARD_FWD=pull)."""
+    "p2p_fwdpull" = the requester-pull forward (TIERSHARD_FWD=pull),
+    "p2p_deferred" = the replica update deferred into the next step
+    (TIERSHARD_REPLICA=deferred)."""
     res = run_case(tmp_path, n_nodes, w, opt, lr_for(n_nodes * w), exchange)
     check_one_step(res, n_nodes, w, opt, lr_for(n_nodes * w))
     if exchange == "p2p_regrow":  # the path was taken, collectively
@@ -242,8 +247,9 @@ def test_inproc_wide_and_narrow_rows(cuda, dim, opt):
     check_one_step(res, 2, 2, opt, lr_for(4), dim=dim)
 
 
-@pytest.mark.parametrize("n_nodes,w,pipelined", [(1, 2, True), (2, 2, False)])
-def test_inproc_stress_ragged_steps(cuda, tmp_path, n_nodes, w, pipelined):
+@pytest.mark.parametrize("n_nodes,w,pipelined,replica", [(1, 2, True, "concurrent"), (2, 2, False, "concurrent"),
+                                                         (2, 2, True, "deferred")])
+def test_inproc_stress_ragged_steps(cuda, tmp_path, n_nodes, w, pipelined, replica):
     """50 host-buffer steps with ragged batches (random sizes, an empty batch
     on one rank, an all-empty step) through the peer-memory protocol on the
     in-process group, a tiny initial receive buffer (regrowth mid-run):
@@ -251,7 +257,7 @@ def test_inproc_stress_ragged_steps(cuda, tmp_path, n_nodes, w, pipelined):
     oracle's 50 sequential updates; replicas stay identical."""
     u, steps = n_nodes * w, 50
     res = mg_worker.run_inproc(n_nodes, w, 1, LR_STEPS, steps=steps, pipelined=pipelined, recv_hint=64,
-                               varying=True)
+                               varying=True, env={"TIERSHARD_REPLICA": replica})
     pb = mg_worker.problem(n_nodes, w, steps=steps, varying=True)
     n, dim, dp = pb["n"], pb["dim"], pb["dp_cut"]
     w_ref = orc.init_table(77, n, dim)
