@@ -427,6 +427,31 @@ struct ts_table {
                                 const tsd::DenseRange& d1);
   void forward(const uint32_t* d_rows, uint64_t occ, float* d_out);
   void backward(const float* d_grad);
+  // ---- cross-step dedup (U = 1, ts_table_train_steps_host) ---------------
+  // The dedup of step s+1 needs only its ids, which the pipelined host path
+  // has on the device one step ahead: it runs on `pre` beside step s's
+  // segment update instead of beside step s+1's gather, so the gather gets
+  // every SM.  Two dedup buffer sets alternate by step parity (the swap
+  // below exchanges the table's members with `alt`); step s+1's dedup waits
+  // for step s's gather to end, by which time step s-1's segment kernels --
+  // the last readers of that set -- have finished.  TIERSHARD_LOOKAHEAD=1
+  // enables it (measured no gain, see create()).
+  struct DedupSet {
+    tsd::DevBuf<uint32_t> keys_a, vals_a, keys_b, vals_b, ghist, goff, sort_counters, starts, seg_keys,
+        seg_scratch, nseg, seg_split, long_list, long_count, piece_off;
+    tsd::DevBuf<uint64_t> sort_status;
+    uint32_t* dd_keys = nullptr;
+    uint32_t* dd_vals = nullptr;
+  } alt;
+  bool lookahead = false, alt_ready = false, skip_fwd_dedup = false;
+  cudaStream_t pre = nullptr;
+  cudaEvent_t ev_pre[2] = {nullptr, nullptr}, ev_gather_done = nullptr;
+  cudaEvent_t ev_dedup_cur = nullptr;  // the event the backward's dedup wait uses
+  unsigned la_gather_grid = 0;
+  void swap_dedup();
+  void dedup_rows(cudaStream_t on, const uint32_t* rows, uint64_t occ);
+  void train_steps_lookahead(uint32_t* const* buf, const uint32_t* const* h_rows, const uint64_t* occ,
+                             uint32_t steps);
   // One training step (forward, then backward with grad = out).  At U = 1
   // with TIERSHARD_GRAPH=1 it is captured into a CUDA graph and replayed:
   // the step's ~20 kernels across the compute and aux streams become one
@@ -505,6 +530,21 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     }
   }
 
+  if (U == 1 && aux) {
+    // measured at C2 (tools/la_ab.sh, tools/la_trace.py): e2e 2.85-2.97 M
+    // with it against 2.87 M without, within noise -- the persistent
+    // segment-update grids hold every SM slot, so step s+1's sort makes
+    // almost no progress beside them (1.25 ms instead of 0.5) and ends up
+    // beside step s+1's gather anyway.  Opt-in (TIERSHARD_LOOKAHEAD=1).
+    const char* le = std::getenv("TIERSHARD_LOOKAHEAD");
+    lookahead = le && std::string(le) == "1";
+    if (lookahead) {
+      TSD_CUDA(cudaStreamCreateWithFlags(&pre, cudaStreamNonBlocking));
+      for (cudaEvent_t* e : {&ev_pre[0], &ev_pre[1], &ev_gather_done}) {
+        TSD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+      }
+    }
+  }
   if (U == 1) {
     // measured at C2, N=1: 3.293 M samples/s with the graph, 3.307 M without
     // (and 2.94 / 2.96 M end to end) -- the step's launches already run ahead
@@ -606,6 +646,14 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     const unsigned per_sm = e ? static_cast<unsigned>(std::max(1, std::atoi(e)))
                               : (gather_bulk_stages ? 5u : (U == 1 ? 6u : 8u));
     fwd_gather_grid = std::min(gather_grid, static_cast<unsigned>(tsd::sm_count()) * per_sm);
+    // with the dedup moved beside the previous step's segment update
+    // (lookahead), the gather runs alone: its fastest grid (bulk 6 x 2:
+    // 0.53 ms per C2 forward; register 8)
+    {
+      const char* le = std::getenv("TIERSHARD_LA_GATHER_BLOCKS");
+      const unsigned la = le ? static_cast<unsigned>(std::max(1, std::atoi(le))) : (gather_bulk_stages ? 6u : 8u);
+      la_gather_grid = std::min(gather_grid, static_cast<unsigned>(tsd::sm_count()) * la);
+    }
     // TIERSHARD_GATHER_GRID: total blocks (fractional blocks per SM, A/B)
     if (const char* ge2 = std::getenv("TIERSHARD_GATHER_GRID")) {
       fwd_gather_grid = std::min(gather_grid, static_cast<unsigned>(std::max(1, std::atoi(ge2))));
@@ -985,18 +1033,103 @@ void ts_table::exchange(const void* send, const std::vector<uint64_t>& s_off,
 
 // U = 1 dedup: stable sort of the forward's row ids (key = canonical row,
 // value = position) and segment heads, on stream `on`.
-void ts_table::dedup_local(cudaStream_t on) {
+void ts_table::dedup_local(cudaStream_t on) { dedup_rows(on, last_rows, last_occ); }
+
+void ts_table::dedup_rows(cudaStream_t on, const uint32_t* rows, uint64_t occ) {
   using namespace tsd;
   RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, ghist.ptr, goff.ptr,
                   sort_status.ptr, sort_counters.ptr};
   const int key_bits = bits_for(local_rows ? local_rows - 1 : 0);
   int t = phase_begin(kPhaseSort, on);
-  radix_sort_pairs(last_rows, nullptr, last_occ, key_bits, rb, &dd_keys, &dd_vals, on);
+  radix_sort_pairs(rows, nullptr, occ, key_bits, rb, &dd_keys, &dd_vals, on);
   phase_end(t);
   t = phase_begin(kPhaseSegments, on);
-  segment_starts(dd_keys, last_occ, starts.ptr, seg_keys.ptr, nseg.ptr, seg_scratch.ptr, on);
+  segment_starts(dd_keys, occ, starts.ptr, seg_keys.ptr, nseg.ptr, seg_scratch.ptr, on);
   TSD_CUDA(cudaMemsetAsync(seg_split.ptr, 0, sizeof(uint32_t), on));  // range [0, nseg)
   phase_end(t);
+}
+
+void ts_table::swap_dedup() {
+  std::swap(keys_a, alt.keys_a);
+  std::swap(vals_a, alt.vals_a);
+  std::swap(keys_b, alt.keys_b);
+  std::swap(vals_b, alt.vals_b);
+  std::swap(ghist, alt.ghist);
+  std::swap(goff, alt.goff);
+  std::swap(sort_counters, alt.sort_counters);
+  std::swap(sort_status, alt.sort_status);
+  std::swap(starts, alt.starts);
+  std::swap(seg_keys, alt.seg_keys);
+  std::swap(seg_scratch, alt.seg_scratch);
+  std::swap(nseg, alt.nseg);
+  std::swap(seg_split, alt.seg_split);
+  std::swap(long_list, alt.long_list);
+  std::swap(long_count, alt.long_count);
+  std::swap(piece_off, alt.piece_off);
+  std::swap(dd_keys, alt.dd_keys);
+  std::swap(dd_vals, alt.dd_vals);
+}
+
+void ts_table::train_steps_lookahead(uint32_t* const* buf, const uint32_t* const* h_rows, const uint64_t* occ,
+                                     uint32_t steps) {
+  using namespace tsd;
+  if (!alt_ready) {  // the second dedup set, sized like the first
+    swap_dedup();
+    ensure_sort_capacity(cfg.max_occurrences);
+    nseg.ensure(4);
+    seg_split.ensure(4);
+    long_count.ensure(4);
+    swap_dedup();
+    alt_ready = true;
+  }
+  const auto stage = [&](uint32_t s) {
+    const int b = static_cast<int>(s & 1u);
+    TSD_CUDA(cudaStreamWaitEvent(copy, ev_consumed[b], 0));
+    if (occ[s]) {
+      TSD_CUDA(cudaMemcpyAsync(buf[b], h_rows[s], sizeof(uint32_t) * occ[s], cudaMemcpyHostToDevice, copy));
+    }
+    TSD_CUDA(cudaEventRecord(ev_copied[b], copy));
+  };
+  const auto prefetch = [&](uint32_t s) {  // dedup of step s into the active set, on `pre`
+    const int b = static_cast<int>(s & 1u);
+    TSD_CUDA(cudaStreamWaitEvent(pre, ev_copied[b], 0));
+    dedup_rows(pre, buf[b], occ[s]);
+    if (long_concurrent) launch_long_segments(starts.ptr, seg_split.ptr, nseg.ptr, occ[s], seg_scratch_view(), pre);
+    TSD_CUDA(cudaEventRecord(ev_pre[b], pre));
+  };
+  if (dedup_ready) {  // a plain forward left its dedup running
+    TSD_CUDA(cudaStreamWaitEvent(stream, ev_dedup, 0));
+    dedup_ready = false;
+  }
+  stage(0);
+  prefetch(0);
+  const unsigned saved_grid = fwd_gather_grid;
+  for (uint32_t s = 0; s < steps; ++s) {
+    const int b = static_cast<int>(s & 1u);
+    if (s + 1 < steps) stage(s + 1);
+    TSD_CUDA(cudaStreamWaitEvent(stream, ev_copied[b], 0));
+    skip_fwd_dedup = true;
+    fwd_gather_grid = la_gather_grid;
+    forward(buf[b], occ[s], host_out.ptr);
+    fwd_gather_grid = saved_grid;
+    skip_fwd_dedup = false;
+    if (s + 1 < steps) {  // step s+1's dedup beside this step's segment update
+      TSD_CUDA(cudaEventRecord(ev_gather_done, stream));
+      swap_dedup();
+      TSD_CUDA(cudaStreamWaitEvent(pre, ev_gather_done, 0));
+      prefetch(s + 1);
+      swap_dedup();
+    }
+    dedup_ready = true;
+    ev_dedup_cur = ev_pre[b];
+    backward(host_out.ptr);
+    ev_dedup_cur = nullptr;
+    TSD_CUDA(cudaEventRecord(ev_consumed[b], stream));
+    TSD_CUDA(cudaMemcpyAsync(h_loss_pinned + s, d_loss.ptr, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    swap_dedup();  // the next step's set becomes the table's
+  }
+  // the table's members hold the set of step `steps` (unused); fine either
+  // way, a later step re-runs its own dedup into whichever set is current
 }
 
 // U > 1 (peer path) dedup: (local row, source) entries of the local
@@ -1058,7 +1191,7 @@ void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
     launch_loss_finalize(loss_partials.ptr, gather_grid, d_loss.ptr, stream);
     n_local_occ = occ;
     n_remote = 0;
-    if (aux) {  // the backward's dedup, overlapping the gather
+    if (aux && !skip_fwd_dedup) {  // the backward's dedup, overlapping the gather
       TSD_CUDA(cudaStreamWaitEvent(aux, ev_fwd0, 0));
       dedup_local(aux);
       TSD_CUDA(cudaEventRecord(ev_dedup, aux));
@@ -1201,7 +1334,7 @@ void ts_table::backward(const float* d_grad) {
     // local id == canonical index: sort the forward's rows directly
     last_entries = occ;
     if (dedup_ready) {
-      TSD_CUDA(cudaStreamWaitEvent(stream, ev_dedup, 0));
+      TSD_CUDA(cudaStreamWaitEvent(stream, ev_dedup_cur ? ev_dedup_cur : ev_dedup, 0));
       dedup_ready = false;
     } else {
       dedup_local(stream);
@@ -1954,6 +2087,7 @@ void ts_table::destroy() {
   if (stream) cudaStreamSynchronize(stream);
   if (aux) cudaStreamSynchronize(aux);
   if (rep) cudaStreamSynchronize(rep);
+  if (pre) cudaStreamSynchronize(pre);
   if (ready && p2p) {
     // peers may still be storing into our exported buffers (replica rows,
     // gradient receive slots): a rendezvous before anything is freed
@@ -2018,6 +2152,16 @@ void ts_table::destroy() {
   if (h_loss_pinned) cudaFreeHost(h_loss_pinned);
   if (comm) cudaStreamDestroy(comm);
   if (rep) cudaStreamDestroy(rep);
+  if (pre) cudaStreamDestroy(pre);
+  for (cudaEvent_t e : {ev_pre[0], ev_pre[1], ev_gather_done}) {
+    if (e) cudaEventDestroy(e);
+  }
+  for (auto* b : {&alt.keys_a, &alt.vals_a, &alt.keys_b, &alt.vals_b, &alt.ghist, &alt.goff, &alt.sort_counters,
+                  &alt.starts, &alt.seg_keys, &alt.seg_scratch, &alt.nseg, &alt.seg_split, &alt.long_list,
+                  &alt.long_count, &alt.piece_off}) {
+    b->release();
+  }
+  alt.sort_status.release();
   for (cudaEvent_t e : {ev_rv, ev_rep}) {
     if (e) cudaEventDestroy(e);
   }
@@ -2172,6 +2316,12 @@ ts_status ts_table_train_steps_host(ts_table* t, const uint32_t* const* h_rows, 
       t->h_loss_cap = cap;
     }
     uint32_t* buf[2] = {t->rows_dev.ptr, t->rows_dev2.ptr};
+    if (t->lookahead && t->U == 1) {
+      t->train_steps_lookahead(buf, h_rows, occ, steps);
+      TSD_CUDA(cudaStreamSynchronize(t->stream));
+      if (h_losses) std::memcpy(h_losses, t->h_loss_pinned, sizeof(double) * steps);
+      return;
+    }
     // step s's ids go to buffer s % 2 on the copy stream once step s-2 (the
     // buffer's last reader) has finished; the copy of step s+1 is queued
     // before step s's compute, so it overlaps it
@@ -2330,6 +2480,7 @@ ts_status ts_table_synchronize(ts_table* t) {
     if (t->aux) TSD_CUDA(cudaStreamSynchronize(t->aux));
     if (t->comm) TSD_CUDA(cudaStreamSynchronize(t->comm));
     if (t->rep) TSD_CUDA(cudaStreamSynchronize(t->rep));
+    if (t->pre) TSD_CUDA(cudaStreamSynchronize(t->pre));
   });
 }
 

@@ -194,8 +194,8 @@ def test_segment_schedules_bit_exact(cuda, monkeypatch, schedule):
     table.close()
 
 
-@pytest.mark.parametrize("graph", ["1", "0"])
-def test_train_steps_graph_bit_exact(cuda, monkeypatch, graph):
+@pytest.mark.parametrize("graph,lookahead", [("1", "0"), ("0", "0"), ("0", "1"), ("1", "1")])
+def test_train_steps_graph_bit_exact(cuda, monkeypatch, graph, lookahead):
     """ts_table_train_step(s)_host at U = 1 with the step captured into a CUDA
     graph (TIERSHARD_GRAPH=1: re-captured every call and updated in place,
     re-instantiated when the topology changes -- e.g. an empty batch) and
@@ -203,6 +203,7 @@ def test_train_steps_graph_bit_exact(cuda, monkeypatch, graph):
     oracle's sequential updates, bit for bit."""
     import paper_2301_02959_b200 as ts
     monkeypatch.setenv("TIERSHARD_GRAPH", graph)
+    monkeypatch.setenv("TIERSHARD_LOOKAHEAD", lookahead)  # cross-step dedup in train_steps_host
     n, dim, lr = 30_000, 128, 0.02
     rng = np.random.default_rng(12)
     sizes = [20_000, 23_000, 0, 17_000, 23_000]
