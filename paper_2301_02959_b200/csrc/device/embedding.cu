@@ -410,7 +410,8 @@ pull_rows_kernel(const uint32_t* __restrict__ sorted_bucket, const uint32_t* __r
 // Fixed-shape tree over the partials (thread t sums t, t+1024, ... in order,
 // then a fixed shared-memory tree): deterministic for a fixed grid.
 __global__ void __launch_bounds__(1024)
-loss_finalize_kernel(const double* __restrict__ partials, unsigned count, double* __restrict__ loss) {
+loss_finalize_kernel(const double* __restrict__ partials, unsigned count, double* __restrict__ loss,
+                     double* __restrict__ mirror) {
   __shared__ double s[1024];
   double acc = 0.0;
   for (unsigned i = threadIdx.x; i < count; i += 1024) acc += partials[i];
@@ -420,7 +421,10 @@ loss_finalize_kernel(const double* __restrict__ partials, unsigned count, double
     if (threadIdx.x < half) s[threadIdx.x] += s[threadIdx.x + half];
     __syncthreads();
   }
-  if (threadIdx.x == 0) *loss = 0.5 * s[0];
+  if (threadIdx.x == 0) {
+    *loss = 0.5 * s[0];
+    if (mirror) *mirror = 0.5 * s[0];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1125,8 +1129,9 @@ void launch_pull_rows(const uint32_t* sorted_bucket, const uint32_t* order, cons
   TSD_LAUNCH_CHECK();
 }
 
-void launch_loss_finalize(const double* partials, unsigned count, double* loss, cudaStream_t stream) {
-  loss_finalize_kernel<<<1, 1024, 0, stream>>>(partials, count, loss);
+void launch_loss_finalize(const double* partials, unsigned count, double* loss, cudaStream_t stream,
+                          double* mirror) {
+  loss_finalize_kernel<<<1, 1024, 0, stream>>>(partials, count, loss, mirror);
   TSD_LAUNCH_CHECK();
 }
 

@@ -97,8 +97,10 @@ void launch_pull_rows(const uint32_t* sorted_bucket, const uint32_t* order, cons
 void set_compute_blocks_per_sm(unsigned per_sm);
 
 // Final fixed-order reduction of the loss partials: *loss = 0.5 * sum.
+// mirror (nullable): a second destination, e.g. a host-mapped pinned slot,
+// written by the same kernel (no copy-engine operation per step).
 void launch_loss_finalize(const double* partials, unsigned count, double* loss,
-                          cudaStream_t stream);
+                          cudaStream_t stream, double* mirror = nullptr);
 
 // Segment reduction + optimizer over sorted (keys, vals) with segment starts.
 // Short segments (<= kPiece entries) are reduced and applied by one warp;

@@ -218,7 +218,9 @@ struct ts_table {
   tsd::DevBuf<uint32_t> rows_dev2;
   cudaStream_t copy = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
-  double* h_loss_pinned = nullptr;
+  double* h_loss_pinned = nullptr;  // host-mapped: the loss kernel writes it directly
+  double* h_loss_dev = nullptr;     // its device alias
+  double* loss_mirror = nullptr;    // this step's slot in it (set by the host-step loops)
   uint32_t h_loss_cap = 0;
   // dedup / sort
   tsd::DevBuf<uint32_t> keys_a, vals_a, keys_b, vals_b, ghist, goff, sort_counters;
@@ -1110,6 +1112,7 @@ void ts_table::train_steps_lookahead(uint32_t* const* buf, const uint32_t* const
     TSD_CUDA(cudaStreamWaitEvent(stream, ev_copied[b], 0));
     skip_fwd_dedup = true;
     fwd_gather_grid = la_gather_grid;
+    loss_mirror = h_loss_dev + s;  // the loss kernel writes the host slot itself
     forward(buf[b], occ[s], host_out.ptr);
     fwd_gather_grid = saved_grid;
     skip_fwd_dedup = false;
@@ -1125,7 +1128,7 @@ void ts_table::train_steps_lookahead(uint32_t* const* buf, const uint32_t* const
     backward(host_out.ptr);
     ev_dedup_cur = nullptr;
     TSD_CUDA(cudaEventRecord(ev_consumed[b], stream));
-    TSD_CUDA(cudaMemcpyAsync(h_loss_pinned + s, d_loss.ptr, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    loss_mirror = nullptr;
     swap_dedup();  // the next step's set becomes the table's
   }
   // the table's members hold the set of step `steps` (unused); fine either
@@ -1188,7 +1191,7 @@ void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
     launch_gather_local(d_rows, occ, d_w, d_out, rv, cfg.dim, loss_partials.ptr, fwd_gather_grid, stream,
                         gather_bulk_stages);
     phase_end(t);
-    launch_loss_finalize(loss_partials.ptr, gather_grid, d_loss.ptr, stream);
+    launch_loss_finalize(loss_partials.ptr, gather_grid, d_loss.ptr, stream, loss_mirror);
     n_local_occ = occ;
     n_remote = 0;
     if (aux && !skip_fwd_dedup) {  // the backward's dedup, overlapping the gather
@@ -1298,7 +1301,7 @@ void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   phase_end(t);
   TSD_CUDA(cudaStreamWaitEvent(stream, ev_fwd, 0));
   // loss = local-gather partials + scatter partials, fixed order
-  launch_loss_finalize(loss_partials.ptr, 2 * gather_grid, d_loss.ptr, stream);
+  launch_loss_finalize(loss_partials.ptr, 2 * gather_grid, d_loss.ptr, stream, loss_mirror);
 }
 
 // ---------------------------------------------------------------------------
@@ -1543,7 +1546,7 @@ void ts_table::forward_p2p_pull(const uint32_t* d_rows, uint64_t occ, float* d_o
   TSD_CUDA(cudaEventRecord(ev_fwd, rs));
   TSD_CUDA(cudaStreamWaitEvent(stream, ev_fwd, 0));
   launch_loss_finalize(loss_partials.ptr, static_cast<unsigned>(gather_grid + remote_loss_slots), d_loss.ptr,
-                       stream);
+                       stream, loss_mirror);
 
   // ---- comm stream, beside the gather: counts, then the request lists -----
   TSD_CUDA(cudaStreamWaitEvent(comm, ev_ids, 0));
@@ -1766,7 +1769,7 @@ void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   }
   TSD_CUDA(cudaStreamWaitEvent(stream, ev_fwd, 0));
   launch_loss_finalize(loss_partials.ptr, static_cast<unsigned>(gather_grid + remote_loss_slots), d_loss.ptr,
-                       stream);
+                       stream, loss_mirror);
 }
 
 // Segments [*d_lo, *d_hi): short ones on the compute stream, long ones listed
@@ -2312,7 +2315,8 @@ ts_status ts_table_train_steps_host(ts_table* t, const uint32_t* const* h_rows, 
       t->h_loss_pinned = nullptr;
       t->h_loss_cap = 0;
       const uint32_t cap = std::max<uint32_t>(steps, 4096);
-      TSD_CUDA(cudaHostAlloc(&t->h_loss_pinned, sizeof(double) * cap, cudaHostAllocDefault));
+      TSD_CUDA(cudaHostAlloc(&t->h_loss_pinned, sizeof(double) * cap, cudaHostAllocMapped));
+      TSD_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&t->h_loss_dev), t->h_loss_pinned, 0));
       t->h_loss_cap = cap;
     }
     uint32_t* buf[2] = {t->rows_dev.ptr, t->rows_dev2.ptr};
@@ -2338,10 +2342,10 @@ ts_status ts_table_train_steps_host(ts_table* t, const uint32_t* const* h_rows, 
       if (s + 1 < steps) stage(s + 1);
       const int b = static_cast<int>(s & 1u);
       TSD_CUDA(cudaStreamWaitEvent(t->stream, t->ev_copied[b], 0));
+      t->loss_mirror = t->h_loss_dev + s;  // the loss kernel writes the host slot itself
       t->train_step(buf[b], occ[s], t->host_out.ptr);
+      t->loss_mirror = nullptr;
       TSD_CUDA(cudaEventRecord(t->ev_consumed[b], t->stream));
-      TSD_CUDA(cudaMemcpyAsync(t->h_loss_pinned + s, t->d_loss.ptr, sizeof(double), cudaMemcpyDeviceToHost,
-                               t->stream));
     }
     TSD_CUDA(cudaStreamSynchronize(t->stream));
     if (h_losses) std::memcpy(h_losses, t->h_loss_pinned, sizeof(double) * steps);
