@@ -41,7 +41,15 @@ void use_device(int device) {
   }
 }
 
+namespace {
+std::atomic<int> g_sm_budget{0};
+}
+
+void set_sm_budget(int sms) { g_sm_budget.store(sms, std::memory_order_relaxed); }
+
 int sm_count() {
+  const int budget = g_sm_budget.load(std::memory_order_relaxed);
+  if (budget > 0) return budget;
   int dev = 0, n = 0;
   TSD_CUDA(cudaGetDevice(&dev));
   TSD_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));

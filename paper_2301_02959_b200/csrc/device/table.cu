@@ -45,6 +45,7 @@
 #include "layout.hpp"
 #include "peer.cuh"
 #include "route.cuh"
+#include "smpart.cuh"
 
 namespace tsd {
 namespace {
@@ -153,6 +154,20 @@ struct ts_table {
   ts_table_config cfg{};
   uint32_t U = 1, W = 1, N = 1, g = 0, slot = 0, node = 0;
   cudaStream_t stream = nullptr;  // compute stream (S)
+  // TIERSHARD_SM_SPLIT=K: green-context SM partition -- the exchange (U > 1:
+  // comm, rep) or dedup (U = 1: aux) streams on K SMs of their own, the
+  // compute streams on the rest (grids sized for it).  allgather_bytes then
+  // runs NCCL on a separate stream of the whole device.
+  tsd::SmPartition smp;
+  cudaStream_t nccl_st = nullptr;
+  cudaStream_t dd = nullptr;  // the prefetched dedup's stream (K partition) when split, else aux
+  cudaStream_t dedup_stream() const { return dd ? dd : aux; }
+  cudaStream_t make_stream(int part, int priority) {
+    if (smp.active()) return tsd::partition_stream(smp, part, priority);
+    cudaStream_t st = nullptr;
+    TSD_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, priority));
+    return st;
+  }
   cudaStream_t comm = nullptr;    // exchange / all-reduce stream (C), U > 1
   // U = 1: the dedup (sort + segment heads) needs only the row ids, so the
   // forward starts it on `aux` beside the gather; the backward waits for it.
@@ -507,7 +522,27 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
   if (c.group && tsd::group_size(c.group) != U) fail(TS_ERR_CONFIG, "table: group size differs from N*W");
   if (U > 1 && !tier_dest) fail(TS_ERR_CONFIG, "table: U > 1 needs the placement table");
   use_device(c.device);
-  TSD_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  {
+    // default at U > 1 with one process per GPU (the flag-barrier peer
+    // path): the exchange streams get 48 SMs (64 with several nodes) of
+    // their own.  Measured at C2 (ms/step, tools/mg_env_ab.sh): N=2 1x2
+    // K=0 2.285, 40 2.231, 48 2.244, 56 2.304, 64 2.425; N=4 1x4 K=0 3.27,
+    // 32 3.10, 40 2.97, 48 2.85-2.90, 64 2.95, 72 3.05; N=4 2x2 3-tier K=0
+    // 3.30, 40 3.33, 48 3.31, 64 3.13.  The persistent HBM grids otherwise
+    // hold every SM slot, and the serve / push / replica / rendezvous
+    // kernels wait for them; at U = 1 a split only slows the dedup sort
+    // and the long-segment path (1.23 -> 1.43-2.31 ms).
+    const char* se = std::getenv("TIERSHARD_SM_SPLIT");
+    const char* xe = std::getenv("TIERSHARD_EXCHANGE");
+    const bool staged = xe && std::string(xe) == "nccl";
+    const int k = se ? std::atoi(se) : ((U > 1 && !c.group && !staged) ? (N > 1 ? 64 : 48) : 0);
+    if (k > 0) {
+      smp = make_partition(c.device, k);
+      set_sm_budget(smp.sms[1]);
+      TSD_CUDA(cudaStreamCreateWithFlags(&nccl_st, cudaStreamNonBlocking));
+    }
+  }
+  stream = make_stream(1, 0);
   seg_short_max = tsd::short_max(U);
   {
     if (const char* e = std::getenv("TIERSHARD_DEDUP_IN_FORWARD")) dedup_in_forward = std::string(e) != "0";
@@ -520,7 +555,12 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
       const bool aux_high = pe ? std::string(pe) == "high" : U == 1;
       int lo_pri = 0, hi_pri = 0;
       TSD_CUDA(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
-      TSD_CUDA(cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, aux_high ? hi_pri : lo_pri));
+      aux = make_stream(1, aux_high ? hi_pri : lo_pri);
+      // TIERSHARD_SM_SPLIT_DEDUP=1: the prefetched dedup on a stream of the
+      // K partition, beside the exchange kernels.  Measured at C2, N=2 with
+      // K = 32 / 40 / 48: 2.79 / 2.53 / 2.37 ms against 2.23 with the
+      // dedup on the rest -- the latency-bound sort needs the SM count
+      if (smp.active() && std::getenv("TIERSHARD_SM_SPLIT_DEDUP")) dd = make_stream(0, hi_pri);
       TSD_CUDA(cudaEventCreateWithFlags(&ev_fwd0, cudaEventDisableTiming));
       TSD_CUDA(cudaEventCreateWithFlags(&ev_dedup, cudaEventDisableTiming));
     }
@@ -541,7 +581,7 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     const char* le = std::getenv("TIERSHARD_LOOKAHEAD");
     lookahead = le && std::string(le) == "1";
     if (lookahead) {
-      TSD_CUDA(cudaStreamCreateWithFlags(&pre, cudaStreamNonBlocking));
+      pre = make_stream(0, 0);
       for (cudaEvent_t* e : {&ev_pre[0], &ev_pre[1], &ev_gather_done}) {
         TSD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
       }
@@ -717,7 +757,7 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     // the persistent compute grids they overlap with
     int lo_prio = 0, hi_prio = 0;
     TSD_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
-    TSD_CUDA(cudaStreamCreateWithPriority(&comm, cudaStreamNonBlocking, hi_prio));
+    comm = make_stream(0, hi_prio);
     for (cudaEvent_t* e : {&ev_ids, &ev_fwd, &ev_bwd0, &ev_grads, &ev_dense, &ev_ar}) {
       TSD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
@@ -746,10 +786,12 @@ std::vector<uint8_t> ts_table::allgather_bytes(const void* mine, size_t bytes) {
     return all;
   }
   xfer.ensure(bytes * U);
-  TSD_CUDA(cudaMemcpyAsync(xfer.ptr + bytes * g, mine, bytes, cudaMemcpyHostToDevice, comm));
-  TSD_NCCL(ncclAllGather(xfer.ptr + bytes * g, xfer.ptr, bytes, ncclUint8, world, comm));
-  TSD_CUDA(cudaMemcpyAsync(all.data(), xfer.ptr, bytes * U, cudaMemcpyDeviceToHost, comm));
-  TSD_CUDA(cudaStreamSynchronize(comm));
+  cudaStream_t ns = nccl_st ? nccl_st : comm;
+  if (nccl_st) TSD_CUDA(cudaStreamSynchronize(comm));  // whatever comm had queued, first
+  TSD_CUDA(cudaMemcpyAsync(xfer.ptr + bytes * g, mine, bytes, cudaMemcpyHostToDevice, ns));
+  TSD_NCCL(ncclAllGather(xfer.ptr + bytes * g, xfer.ptr, bytes, ncclUint8, world, ns));
+  TSD_CUDA(cudaMemcpyAsync(all.data(), xfer.ptr, bytes * U, cudaMemcpyDeviceToHost, ns));
+  TSD_CUDA(cudaStreamSynchronize(ns));
   return all;
 }
 
@@ -827,6 +869,9 @@ void ts_table::setup_p2p() {
     if (!v) ok = 0;
   }
   p2p = ok != 0;
+  if (!p2p && smp.active()) {
+    fail(TS_ERR_CONFIG, "table: the SM partition needs the peer-memory exchange (set TIERSHARD_SM_SPLIT=0)");
+  }
   if (!p2p) return;
   if (const char* env = std::getenv("TIERSHARD_REPLICA")) replica_concurrent = std::string(env) != "serial";
   if (const char* env = std::getenv("TIERSHARD_GRADS")) grads_push = std::string(env) != "pull";
@@ -889,15 +934,16 @@ void ts_table::setup_p2p() {
   flag_barrier.me = static_cast<int>(g);
   if (!grp) {  // in-process ranks may share a GPU: a spinning block could starve a peer
     const char* be = std::getenv("TIERSHARD_BARRIER");
-    flag_barriers = !(be && std::string(be) == "nccl");
+    flag_barriers = !(be && std::string(be) == "nccl") || smp.active();
     const char* ce = std::getenv("TIERSHARD_FWD_COUNTS");
-    mailbox_counts = flag_barriers && ce && std::string(ce) == "mailbox";
+    // with an SM partition the step keeps NCCL off the (green) comm stream
+    mailbox_counts = flag_barriers && ((ce && std::string(ce) == "mailbox") || smp.active());
   }
   replica_deferred = replica_deferred && (flag_barriers || grp);
   if (replica_deferred) {
     int lo_prio = 0, hi_prio = 0;
     TSD_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
-    TSD_CUDA(cudaStreamCreateWithPriority(&rep, cudaStreamNonBlocking, hi_prio));
+    rep = make_stream(0, hi_prio);
     TSD_CUDA(cudaEventCreateWithFlags(&ev_rv, cudaEventDisableTiming));
     TSD_CUDA(cudaEventCreateWithFlags(&ev_rep, cudaEventDisableTiming));
   }
@@ -1195,11 +1241,13 @@ void ts_table::forward(const uint32_t* d_rows, uint64_t occ, float* d_out) {
     n_local_occ = occ;
     n_remote = 0;
     if (aux && !skip_fwd_dedup) {  // the backward's dedup, overlapping the gather
-      TSD_CUDA(cudaStreamWaitEvent(aux, ev_fwd0, 0));
-      dedup_local(aux);
-      TSD_CUDA(cudaEventRecord(ev_dedup, aux));
+      cudaStream_t ds = dedup_stream();
+      TSD_CUDA(cudaStreamWaitEvent(ds, ev_fwd0, 0));
+      dedup_local(ds);
+      TSD_CUDA(cudaEventRecord(ev_dedup, ds));
       // the long-segment list is needed only by the backward's aux work: it
       // stays off the chain the short-segment kernel waits for
+      if (ds != aux) TSD_CUDA(cudaStreamWaitEvent(aux, ev_dedup, 0));
       if (long_concurrent) launch_long_segments(starts.ptr, seg_split.ptr, nseg.ptr, occ, seg_scratch_view(), aux);
       dedup_ready = true;
     }
@@ -1611,9 +1659,9 @@ void ts_table::forward_p2p_pull(const uint32_t* d_rows, uint64_t occ, float* d_o
   phase_end(t);
   if (aux) {  // the backward's dedup needs only the ids
     TSD_CUDA(cudaEventRecord(ev_fwd0, comm));
-    TSD_CUDA(cudaStreamWaitEvent(aux, ev_fwd0, 0));
-    dedup_p2p(aux);
-    TSD_CUDA(cudaEventRecord(ev_dedup, aux));
+    TSD_CUDA(cudaStreamWaitEvent(dedup_stream(), ev_fwd0, 0));
+    dedup_p2p(dedup_stream());
+    TSD_CUDA(cudaEventRecord(ev_dedup, dedup_stream()));
     dedup_ready = true;
   }
 }
@@ -1748,9 +1796,9 @@ void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   launch_pull_requests(pt, recv_ids.ptr, recv_pos.ptr, comm);
   if (aux) {  // the backward's dedup needs only the ids: overlap it with the gather / serve
     TSD_CUDA(cudaEventRecord(ev_fwd0, comm));
-    TSD_CUDA(cudaStreamWaitEvent(aux, ev_fwd0, 0));
-    dedup_p2p(aux);
-    TSD_CUDA(cudaEventRecord(ev_dedup, aux));
+    TSD_CUDA(cudaStreamWaitEvent(dedup_stream(), ev_fwd0, 0));
+    dedup_p2p(dedup_stream());
+    TSD_CUDA(cudaEventRecord(ev_dedup, dedup_stream()));
     dedup_ready = true;
   }
   // served Flex rows replicated across nodes are written by the deferred
@@ -2091,6 +2139,7 @@ void ts_table::destroy() {
   if (aux) cudaStreamSynchronize(aux);
   if (rep) cudaStreamSynchronize(rep);
   if (pre) cudaStreamSynchronize(pre);
+  if (dd) cudaStreamSynchronize(dd);
   if (ready && p2p) {
     // peers may still be storing into our exported buffers (replica rows,
     // gradient receive slots): a rendezvous before anything is freed
@@ -2169,6 +2218,9 @@ void ts_table::destroy() {
     if (e) cudaEventDestroy(e);
   }
   if (stream) cudaStreamDestroy(stream);
+  if (nccl_st) cudaStreamDestroy(nccl_st);
+  if (dd) cudaStreamDestroy(dd);
+  tsd::destroy_partition(smp);
 }
 
 // ---------------------------------------------------------------------------
@@ -2473,7 +2525,7 @@ ts_status ts_table_synchronize(ts_table* t) {
       // collective: peers store into our replicated rows and receive
       // buffers, so "our step is done" means every rank's step is done --
       // a rendezvous behind all of this rank's streams, then wait for it
-      for (cudaStream_t s : {t->stream, t->aux, t->rep}) {
+      for (cudaStream_t s : {t->stream, t->aux, t->rep, t->dd}) {
         if (!s) continue;
         TSD_CUDA(cudaEventRecord(t->ev_ar, s));
         TSD_CUDA(cudaStreamWaitEvent(t->comm, t->ev_ar, 0));
@@ -2485,6 +2537,7 @@ ts_status ts_table_synchronize(ts_table* t) {
     if (t->comm) TSD_CUDA(cudaStreamSynchronize(t->comm));
     if (t->rep) TSD_CUDA(cudaStreamSynchronize(t->rep));
     if (t->pre) TSD_CUDA(cudaStreamSynchronize(t->pre));
+    if (t->dd) TSD_CUDA(cudaStreamSynchronize(t->dd));
   });
 }
 
