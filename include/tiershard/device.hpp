@@ -23,6 +23,7 @@
 struct ts_table;   // C-ABI handles
 struct ts_keymap;
 struct ts_sampler;
+struct ts_group;
 
 namespace tiershard {
 
@@ -33,6 +34,24 @@ using NcclUniqueId = std::array<uint8_t, 128>;
 // Fresh communicator id: rank 0 calls it and ships it to the other ranks.
 NcclUniqueId new_nccl_unique_id();
 
+// In-process rank group: all N*W ranks as host threads of one process (any
+// GPUs, several per GPU allowed), instead of one process per GPU over NCCL.
+// Each rank's SequenceEmbedding is created, stepped and destroyed by its own
+// thread; destroy the group after its tables.  abort() makes every pending
+// collective of its tables fail at once (a rank's thread failed).
+class DeviceGroup {
+ public:
+  explicit DeviceGroup(uint32_t ranks);
+  ~DeviceGroup();
+  DeviceGroup(const DeviceGroup&) = delete;
+  DeviceGroup& operator=(const DeviceGroup&) = delete;
+  void abort();
+  ts_group* handle() const { return group_; }
+
+ private:
+  ts_group* group_ = nullptr;
+};
+
 struct DeviceOptions {
   int device = 0;
   uint32_t rank = 0;                 // this process's GPU index in [0, N*W)
@@ -41,7 +60,12 @@ struct DeviceOptions {
   float learning_rate = 0.01f;
   float epsilon = 1e-8f;
   uint64_t max_occurrences = uint64_t{1} << 22;  // per step, this rank
-  const NcclUniqueId* nccl_id = nullptr;         // required when N*W > 1
+  const NcclUniqueId* nccl_id = nullptr;         // N*W > 1, one process per GPU
+  const DeviceGroup* group = nullptr;            // N*W > 1, all ranks in this process
+  // capacity (rows) of the buffer peers push this rank's remote gradients
+  // into: e.g. the plan's expected remote occurrences + 25 %; 0 = the worst
+  // case, (N*W-1) x max_occurrences.  A step that needs more grows it.
+  uint64_t recv_rows_hint = 0;
 };
 
 // The per-row placement byte the planner emits for the device: RW owner
@@ -153,6 +177,11 @@ class SequenceEmbedding {
   void backward(const float* d_grad);
   // Host-buffer step: copy, forward, loss 0.5*|out|^2, backward, read loss.
   double train_step_host(const std::vector<uint32_t>& rows);
+  // The same over several batches in one call, each step's host-to-device
+  // copy overlapping the previous step (pinned host memory copies
+  // asynchronously); returns one loss per batch.
+  std::vector<double> train_steps_host(const std::vector<const uint32_t*>& rows,
+                                       const std::vector<uint64_t>& occurrences);
 
   // This rank's column of the reference's 7 x U counter block
   // (send/recv global, send/recv intra, dp_local, served, distinct).

@@ -70,7 +70,26 @@ void SequenceEmbedding::create(uint64_t n_rows, uint64_t dp_cut, uint64_t flex_c
   c.eps = options.epsilon;
   c.max_occurrences = options.max_occurrences;
   c.nccl_unique_id = options.nccl_id ? options.nccl_id->data() : nullptr;
+  c.group = options.group ? options.group->handle() : nullptr;
+  c.recv_rows_hint = options.recv_rows_hint;
   detail::check(ts_table_create(&table_, &c, dest.data()));
+}
+
+DeviceGroup::DeviceGroup(uint32_t ranks) { detail::check(ts_group_create(&group_, ranks)); }
+
+DeviceGroup::~DeviceGroup() {
+  if (group_) ts_group_destroy(group_);
+}
+
+void DeviceGroup::abort() { detail::check(ts_group_abort(group_)); }
+
+std::vector<double> SequenceEmbedding::train_steps_host(const std::vector<const uint32_t*>& rows,
+                                                        const std::vector<uint64_t>& occurrences) {
+  if (rows.size() != occurrences.size()) throw ConfigError("train_steps_host: rows / occurrences size mismatch");
+  std::vector<double> losses(rows.size());
+  detail::check(ts_table_train_steps_host(table_, rows.data(), occurrences.data(),
+                                          static_cast<uint32_t>(rows.size()), losses.data()));
+  return losses;
 }
 
 SequenceEmbedding::~SequenceEmbedding() {

@@ -98,3 +98,20 @@ def test_cpp_example_trains_on_device(cuda):
     doc = json.loads(proc.stdout.strip().splitlines()[-1])
     assert doc["occurrences"] > 0 and doc["served"] > 0
     assert doc["last_loss"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nodes,w", [(1, 2), (2, 2)])
+def test_cpp_example_in_process_group(cuda, nodes, w):
+    """The C++ front door with a DeviceGroup: U ranks as threads of one
+    process (tiershard::DeviceGroup, DeviceOptions::group), every rank
+    stepping its slice of the reference Workload through train_steps_host;
+    the summed SERVED counters equal the last iteration's occurrences."""
+    import json
+    proc = subprocess.run([str(EXAMPLE), "--group", str(nodes), str(w), "50000", "3"], capture_output=True,
+                          text=True, timeout=300)
+    assert proc.returncode == 0, proc.stdout + proc.stderr
+    doc = json.loads(proc.stdout.strip().splitlines()[-1])
+    assert doc["ranks"] == nodes * w
+    assert doc["served"] == doc["last_iteration_occurrences"] > 0
+    assert doc["last_loss_sum"] > 0
