@@ -549,10 +549,11 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     if (dedup_in_forward) {
       // aux priority (TIERSHARD_AUX_PRIORITY=high|low): at U = 1 the dedup
       // sort's blocks are dispatched ahead of the gather's (measured at C2
-      // with 6 gather blocks per SM: 1.328 -> 1.307 ms/step); at U > 1 the
-      // comm stream holds the high priority
+      // with 6 gather blocks per SM: 1.328 -> 1.307 ms/step); at U > 1 with
+      // the SM partition too (the comm stream has SMs of its own), beside a
+      // 4-blocks-per-SM gather: N=2 2.21 -> 2.17, N=4 2.86 -> 2.82 ms (medians)
       const char* pe = std::getenv("TIERSHARD_AUX_PRIORITY");
-      const bool aux_high = pe ? std::string(pe) == "high" : U == 1;
+      const bool aux_high = pe ? std::string(pe) == "high" : (U == 1 || smp.active());
       int lo_pri = 0, hi_pri = 0;
       TSD_CUDA(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
       aux = make_stream(1, aux_high ? hi_pri : lo_pri);
@@ -714,11 +715,13 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     const char* e = std::getenv("TIERSHARD_GATHER_BLOCKS");
     // register gather: 6 blocks per SM leave the dedup sort room beside the
     // gather (C2, N=1: 8 -> 1.318 ms/step, 6 -> 1.307, 4 -> 1.328; aux at
-    // high priority).  At U > 1 8 stays best (N=2: 2.33 ms against
-    // 2.35-2.36 with 6; a high-priority aux there costs 0.1 ms: the sort
-    // then delays serve and push).  Bulk gather: 5 (above).
+    // high priority).  At U > 1 without the SM partition 8 (N=2: 2.33 ms
+    // against 2.35-2.36 with 6; a high-priority aux there costs 0.1 ms: the
+    // sort then delays serve and push); with it 4 and a high-priority aux
+    // (N=2 medians 2.21 / 2.17 / 2.24 / 2.42 ms with 8 / 4 / 3 / 2, 6: 2.26;
+    // tools/mg_env_ab.sh).  Bulk gather: 5 (above).
     const unsigned per_sm = e ? static_cast<unsigned>(std::max(1, std::atoi(e)))
-                              : (gather_bulk_stages ? 5u : (U == 1 ? 6u : 8u));
+                              : (gather_bulk_stages ? 5u : (U == 1 ? 6u : (smp.active() ? 4u : 8u)));
     fwd_gather_grid = std::min(gather_grid, static_cast<unsigned>(tsd::sm_count()) * per_sm);
     // with the dedup moved beside the previous step's segment update
     // (lookahead), the gather runs alone: its fastest grid (bulk 6 x 2:
