@@ -150,6 +150,184 @@ scatter_rows_loss_kernel(const float* __restrict__ src, float* __restrict__ dst,
   }
 }
 
+// ---- fused route (launch_route_buckets) -------------------------------------
+constexpr int kRouteThreads = 512;
+constexpr int kRouteWarps = kRouteThreads / 32;
+constexpr int kRouteItems = 8;
+constexpr uint32_t kRouteTile = kRouteThreads * kRouteItems;  // occurrences per block: 8 chunks of 512
+
+__device__ __forceinline__ uint32_t route_bucket(uint32_t c, const BucketView& bv, uint32_t local_bucket,
+                                                 int* tier) {
+  if (c < bv.dp_cut) {
+    *tier = 2;
+    return local_bucket;
+  }
+  const uint32_t d = __ldg(bv.dest + c);
+  if (c < bv.flex_cut) {
+    *tier = 1;
+    return d == bv.slot ? local_bucket : bv.u + d;
+  }
+  *tier = 0;
+  return d == bv.rank ? local_bucket : d;
+}
+
+// hist[b * tiles + tile] = occurrences of bucket b in the tile
+__global__ void __launch_bounds__(kRouteThreads)
+route_hist_kernel(const uint32_t* __restrict__ rows, uint64_t occ, BucketView bv, uint32_t nb,
+                  uint32_t* __restrict__ hist, unsigned long long* __restrict__ tier_counts) {
+  __shared__ unsigned s_cnt[kRouteMaxBuckets];
+  __shared__ unsigned s_tier[3];
+  const uint32_t tiles = static_cast<uint32_t>(gridDim.x);
+  for (uint32_t b = threadIdx.x; b < kRouteMaxBuckets; b += kRouteThreads) s_cnt[b] = 0;
+  if (threadIdx.x < 3) s_tier[threadIdx.x] = 0;
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31u;
+  const uint32_t local_bucket = nb - 1;
+  unsigned tc[3] = {0, 0, 0};
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRouteTile + threadIdx.x;
+  // every load of the thread's kRouteItems occurrences in flight at once
+  uint32_t c[kRouteItems], b[kRouteItems];
+#pragma unroll
+  for (int k = 0; k < kRouteItems; ++k) {
+    const uint64_t i = base + static_cast<uint64_t>(k) * kRouteThreads;
+    c[k] = i < occ ? __ldg(rows + i) : 0;
+  }
+#pragma unroll
+  for (int k = 0; k < kRouteItems; ++k) {
+    const uint64_t i = base + static_cast<uint64_t>(k) * kRouteThreads;
+    b[k] = kRouteMaxBuckets;  // sentinel: past the batch
+    if (i < occ) {
+      int tier;
+      b[k] = route_bucket(c[k], bv, local_bucket, &tier);
+      ++tc[tier];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kRouteItems; ++k) {
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, b[k]);
+    if (b[k] < kRouteMaxBuckets && lane == static_cast<unsigned>(__ffs(peers) - 1)) {
+      atomicAdd(&s_cnt[b[k]], __popc(peers));
+    }
+  }
+  for (int t = 0; t < 3; ++t) {
+    unsigned v = tc[t];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if (lane == 0 && v) atomicAdd(&s_tier[t], v);
+  }
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < nb; b += kRouteThreads) {
+    hist[static_cast<uint64_t>(b) * tiles + blockIdx.x] = s_cnt[b];
+  }
+  if (threadIdx.x < 3 && s_tier[threadIdx.x]) {
+    atomicAdd(tier_counts + threadIdx.x, static_cast<unsigned long long>(s_tier[threadIdx.x]));
+  }
+}
+
+// In-place exclusive scan of hist[0..n) (one block), starts[b] = hist[b *
+// tiles] after it, starts[nb] = occ.
+__global__ void __launch_bounds__(1024)
+route_scan_kernel(uint32_t* __restrict__ hist, uint64_t tiles, uint32_t nb, uint32_t occ,
+                  uint32_t* __restrict__ starts) {
+  __shared__ uint32_t s_warp[32];
+  const uint64_t n = tiles * nb;
+  const uint64_t per = (n + blockDim.x - 1) / blockDim.x;
+  const uint64_t lo = min(n, per * threadIdx.x), hi = min(n, lo + per);
+  uint32_t sum = 0;
+  for (uint64_t j = lo; j < hi; ++j) sum += hist[j];
+  // block exclusive scan of the per-thread sums
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint32_t incl = sum;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= static_cast<unsigned>(o)) incl += v;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < (blockDim.x >> 5) ? s_warp[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, w, o);
+      if (lane >= static_cast<unsigned>(o)) w += v;
+    }
+    s_warp[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  uint32_t run = incl - sum + (warp ? s_warp[warp - 1] : 0);
+  for (uint64_t j = lo; j < hi; ++j) {
+    const uint32_t v = hist[j];
+    hist[j] = run;
+    run += v;
+  }
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b <= nb; b += blockDim.x) {
+    starts[b] = (b < nb && tiles) ? hist[static_cast<uint64_t>(b) * tiles] : (b < nb ? 0u : occ);
+  }
+}
+
+__global__ void __launch_bounds__(kRouteThreads)
+route_scatter_kernel(const uint32_t* __restrict__ rows, uint64_t occ, BucketView bv, uint32_t nb,
+                     const uint32_t* __restrict__ hist, uint32_t* __restrict__ order,
+                     const uint32_t* __restrict__ local, uint32_t* __restrict__ ids) {
+  __shared__ uint32_t s_base[kRouteMaxBuckets];              // next position per bucket
+  __shared__ uint32_t s_wcnt[kRouteWarps][kRouteMaxBuckets];  // chunk counts -> warp offsets
+  const uint32_t tiles = static_cast<uint32_t>(gridDim.x);
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t local_bucket = nb - 1;
+  for (uint32_t b = threadIdx.x; b < nb; b += kRouteThreads) {
+    s_base[b] = hist[static_cast<uint64_t>(b) * tiles + blockIdx.x];
+  }
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRouteTile;
+  // loads first (rows, destinations, remote ids), all in flight at once
+  uint32_t bk[kRouteItems], id[kRouteItems];
+#pragma unroll
+  for (int k = 0; k < kRouteItems; ++k) {
+    const uint64_t i = base + static_cast<uint64_t>(k) * kRouteThreads + threadIdx.x;
+    id[k] = i < occ ? __ldg(rows + i) : 0;
+  }
+#pragma unroll
+  for (int k = 0; k < kRouteItems; ++k) {
+    const uint64_t i = base + static_cast<uint64_t>(k) * kRouteThreads + threadIdx.x;
+    int tier;
+    bk[k] = i < occ ? route_bucket(id[k], bv, local_bucket, &tier) : kRouteMaxBuckets;
+  }
+#pragma unroll
+  for (int k = 0; k < kRouteItems; ++k) {
+    if (bk[k] < local_bucket) id[k] = __ldg(local + id[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < kRouteItems; ++k) {
+    const uint32_t k0 = static_cast<uint32_t>(k) * kRouteThreads;
+    if (base + k0 >= occ) break;  // uniform over the block
+    for (uint32_t e = threadIdx.x; e < kRouteWarps * kRouteMaxBuckets; e += kRouteThreads) {
+      (&s_wcnt[0][0])[e] = 0;
+    }
+    __syncthreads();
+    const uint64_t i = base + k0 + threadIdx.x;
+    const bool valid = i < occ;
+    const uint32_t b = bk[k];
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, b);
+    const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+    if (valid && lane == static_cast<unsigned>(__ffs(peers) - 1)) s_wcnt[warp][b] = __popc(peers);
+    __syncthreads();
+    for (uint32_t bb = threadIdx.x; bb < nb; bb += kRouteThreads) {  // warp offsets, bucket bb
+      uint32_t run = s_base[bb];
+      for (int w = 0; w < kRouteWarps; ++w) {
+        const uint32_t v = s_wcnt[w][bb];
+        s_wcnt[w][bb] = run;
+        run += v;
+      }
+      s_base[bb] = run;
+    }
+    __syncthreads();
+    if (valid) {
+      const uint32_t pos = s_wcnt[warp][b] + rank;
+      order[pos] = static_cast<uint32_t>(i);
+      if (b != local_bucket) ids[pos] = id[k];
+    }
+    __syncthreads();
+  }
+}
+
 unsigned grid_for(uint64_t n, unsigned per_block) {
   const uint64_t want = (n + per_block - 1) / per_block;
   const uint64_t cap = static_cast<uint64_t>(sm_count()) * 16;
@@ -157,6 +335,30 @@ unsigned grid_for(uint64_t n, unsigned per_block) {
 }
 
 }  // namespace
+
+uint64_t route_hist_elems(uint64_t occ, uint32_t nb) {
+  return std::max<uint64_t>(1, (occ + kRouteTile - 1) / kRouteTile) * nb;
+}
+
+void launch_route_buckets(const uint32_t* rows, uint64_t occ, const BucketView& bv, uint32_t nb, uint32_t* hist,
+                          uint32_t* order, uint32_t* starts, const uint32_t* local, uint32_t* ids,
+                          unsigned long long* tier_counts, cudaStream_t stream) {
+  if (nb == 0 || nb > kRouteMaxBuckets) fail(TS_ERR_CONFIG, "route: bucket count out of range");
+  const uint64_t tiles = (occ + kRouteTile - 1) / kRouteTile;
+  if (tiles > 0x7FFFFFFFu) fail(TS_ERR_VALIDATION, "route: batch too large");
+  if (tiles) {
+    route_hist_kernel<<<static_cast<unsigned>(tiles), kRouteThreads, 0, stream>>>(rows, occ, bv, nb, hist,
+                                                                                 tier_counts);
+    TSD_LAUNCH_CHECK();
+  }
+  route_scan_kernel<<<1, 1024, 0, stream>>>(hist, tiles, nb, static_cast<uint32_t>(occ), starts);
+  TSD_LAUNCH_CHECK();
+  if (tiles) {
+    route_scatter_kernel<<<static_cast<unsigned>(tiles), kRouteThreads, 0, stream>>>(rows, occ, bv, nb, hist,
+                                                                                    order, local, ids);
+    TSD_LAUNCH_CHECK();
+  }
+}
 
 void launch_bucket_starts(const uint32_t* hist_scan, uint64_t tiles, uint32_t nb, uint32_t occ,
                           uint32_t* out, cudaStream_t stream) {

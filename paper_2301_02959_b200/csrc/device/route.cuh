@@ -35,6 +35,19 @@ void launch_remote_ids_upto(const uint32_t* rows, const uint32_t* order, uint64_
                             const uint32_t* d_count, const uint32_t* local, uint32_t* ids,
                             cudaStream_t stream);
 
+// The whole route in three kernels, no sort (nb <= kRouteMaxBuckets):
+// per-tile bucket histograms (+ the tier counts), one scan of them
+// (bucket-major) that also writes starts[0..nb] (starts[nb] = occ), and a
+// stable scatter -- warp match ranks within each 512-occurrence chunk of a
+// tile -- that writes order[] (occurrences stably by bucket, the order the
+// counting sort gives) and, for the remote buckets, ids[j] = local id of
+// rows[order[j]] at its server.  `hist` holds route_hist_elems(occ, nb).
+constexpr uint32_t kRouteMaxBuckets = 32;
+uint64_t route_hist_elems(uint64_t occ, uint32_t nb);
+void launch_route_buckets(const uint32_t* rows, uint64_t occ, const BucketView& bv, uint32_t nb, uint32_t* hist,
+                          uint32_t* order, uint32_t* starts, const uint32_t* local, uint32_t* ids,
+                          unsigned long long* tier_counts, cudaStream_t stream);
+
 // dst[dst_idx ? dst_idx[j] : j] = src[src_idx ? src_idx[j] : j] for j < count
 // (rows of `dim` floats).
 void launch_copy_rows(const float* src, const uint32_t* src_idx, float* dst,

@@ -245,6 +245,9 @@ struct ts_table {
   tsd::DevBuf<float> partials;
   // U > 1 routing / exchange
   tsd::DevBuf<uint32_t> bucket, order, send_ids, recv_ids, bucket_start, all_counts;
+  tsd::DevBuf<uint32_t> route_hist;  // per-tile bucket counts (launch_route_buckets)
+  // TIERSHARD_ROUTE=sort: the peer path's route as bucket keys + radix sort
+  bool route_sort = false;
   tsd::DevBuf<float> send_rows, recv_rows, dense_dp, dense_flex;
   tsd::DevBuf<uint32_t> stamp_dp, stamp_flex;  // per dense row: last epoch written (P2P)
   uint32_t epoch = 0;                          // backward steps (P2P)
@@ -756,6 +759,7 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     entry_keys.ensure(max_entries);
     entry_vals.ensure(max_entries);
     bucket.ensure(c.max_occurrences);
+    route_hist.ensure(tsd::route_hist_elems(c.max_occurrences, nb()));
     order.ensure(c.max_occurrences);
     send_ids.ensure(c.max_occurrences);
     // received gradient rows: peers store into this buffer (P2P push), so
@@ -983,6 +987,8 @@ void ts_table::setup_p2p() {
     TSD_CUDA(cudaEventCreateWithFlags(&ev_rep, cudaEventDisableTiming));
   }
   {
+    const char* re = std::getenv("TIERSHARD_ROUTE");
+    route_sort = re && std::string(re) == "sort";
     const char* fe = std::getenv("TIERSHARD_FWD");
     pull_forward = fe && std::string(fe) == "pull" && (flag_barriers || grp) && U <= kMaxGradPeers;
   }
@@ -1721,17 +1727,22 @@ void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
   bv.w = W;
   bv.rank = g;
   bv.slot = slot;
-  launch_bucket_keys(d_rows, occ, bv, bucket.ptr, tier_counts.ptr, stream);
-  RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, ghist.ptr, goff.ptr,
-                  sort_status.ptr, sort_counters.ptr};
-  uint32_t* sorted_b = nullptr;
-  uint32_t* sorted_i = nullptr;
-  radix_sort_pairs(bucket.ptr, nullptr, occ, bits_for(nb() - 1), rb, &sorted_b, &sorted_i, stream);
-  TSD_CUDA(cudaMemcpyAsync(order.ptr, sorted_i, sizeof(uint32_t) * occ, cudaMemcpyDeviceToDevice, stream));
   uint32_t* my_starts = reinterpret_cast<uint32_t*>(my_slot);
-  launch_bucket_starts(goff.ptr, 1, nb(), static_cast<uint32_t>(occ), my_starts, stream);
-  // ids of the remote prefix (the local bucket is last; its count is on the device)
-  launch_remote_ids_upto(d_rows, order.ptr, occ, my_starts + (U + W), d_local, send_ids.ptr, stream);
+  if (route_sort) {  // TIERSHARD_ROUTE=sort: bucket keys + the radix sort (round 1)
+    launch_bucket_keys(d_rows, occ, bv, bucket.ptr, tier_counts.ptr, stream);
+    RadixBuffers rb{keys_a.ptr, vals_a.ptr, keys_b.ptr, vals_b.ptr, ghist.ptr, goff.ptr,
+                    sort_status.ptr, sort_counters.ptr};
+    uint32_t* sorted_b = nullptr;
+    uint32_t* sorted_i = nullptr;
+    radix_sort_pairs(bucket.ptr, nullptr, occ, bits_for(nb() - 1), rb, &sorted_b, &sorted_i, stream);
+    TSD_CUDA(cudaMemcpyAsync(order.ptr, sorted_i, sizeof(uint32_t) * occ, cudaMemcpyDeviceToDevice, stream));
+    launch_bucket_starts(goff.ptr, 1, nb(), static_cast<uint32_t>(occ), my_starts, stream);
+    // ids of the remote prefix (the local bucket is last; its count is on the device)
+    launch_remote_ids_upto(d_rows, order.ptr, occ, my_starts + (U + W), d_local, send_ids.ptr, stream);
+  } else {  // histogram, scan, stable scatter with the remote ids fused
+    launch_route_buckets(d_rows, occ, bv, nb(), route_hist.ptr, order.ptr, my_starts, d_local, send_ids.ptr,
+                         tier_counts.ptr, stream);
+  }
   my_export = export_ptr(d_out);
   TSD_CUDA(cudaMemcpyAsync(my_slot + starts_bytes, &my_export, sizeof(IpcExport), cudaMemcpyHostToDevice,
                            stream));
