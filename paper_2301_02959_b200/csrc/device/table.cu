@@ -309,6 +309,7 @@ struct ts_table {
   uint32_t per_dp = 0, per_flex = 0;  // replicated rows owned per group member
   std::vector<float*> peer_w, peer_state;           // peers' shards (mapped)
   tsd::IpcExport my_export{};                       // staging for the step payload
+  bool export_in_slot = false;                      // my_export is in our payload slot
   uint64_t remote_loss_slots = 0;                   // U * kServeGrid
   // schedule knobs (env, read at creation; defaults = fastest measured):
   //   TIERSHARD_REPLICA=serial|concurrent  replica update after the DP
@@ -825,6 +826,7 @@ std::vector<uint8_t> ts_table::allgather_bytes(const void* mine, size_t bytes) {
     return all;
   }
   xfer.ensure(bytes * U);
+  export_in_slot = false;  // the step payload's slot may live in xfer
   cudaStream_t ns = nccl_st ? nccl_st : comm;
   if (nccl_st) TSD_CUDA(cudaStreamSynchronize(comm));  // whatever comm had queued, first
   TSD_CUDA(cudaMemcpyAsync(xfer.ptr + bytes * g, mine, bytes, cudaMemcpyHostToDevice, ns));
@@ -1743,9 +1745,16 @@ void ts_table::forward_p2p(const uint32_t* d_rows, uint64_t occ, float* d_out) {
     launch_route_buckets(d_rows, occ, bv, nb(), route_hist.ptr, order.ptr, my_starts, d_local, send_ids.ptr,
                          tier_counts.ptr, stream);
   }
-  my_export = export_ptr(d_out);
-  TSD_CUDA(cudaMemcpyAsync(my_slot + starts_bytes, &my_export, sizeof(IpcExport), cudaMemcpyHostToDevice,
-                           stream));
+  {  // the slot keeps the export between steps: rewrite it only when the
+     // output moves (a copy-engine op between the route kernels otherwise)
+    const IpcExport e = export_ptr(d_out);
+    if (!export_in_slot || std::memcmp(&e, &my_export, sizeof(e)) != 0) {
+      my_export = e;
+      TSD_CUDA(cudaMemcpyAsync(my_slot + starts_bytes, &my_export, sizeof(IpcExport), cudaMemcpyHostToDevice,
+                               stream));
+      export_in_slot = true;
+    }
+  }
   phase_end(t);
 
   // ---- one all-gather: every rank's bucket starts + output export --------
