@@ -568,7 +568,19 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
       // K partition, beside the exchange kernels.  Measured at C2, N=2 with
       // K = 32 / 40 / 48: 2.79 / 2.53 / 2.37 ms against 2.23 with the
       // dedup on the rest -- the latency-bound sort needs the SM count
-      if (smp.active() && std::getenv("TIERSHARD_SM_SPLIT_DEDUP")) dd = make_stream(0, hi_pri);
+      // TIERSHARD_SM_SPLIT_DEDUP=device (default at U = 2): on a stream of
+      // the whole device (primary context), free to use either partition's
+      // idle SMs.  Medians: 1x2 2.108 -> 2.087 ms; 1x4 2.70 -> 2.74 (the
+      // sort then delays serve and push there), so U = 2 only
+      const char* de = std::getenv("TIERSHARD_SM_SPLIT_DEDUP");
+      if (!de && U == 2 && N == 1) de = "device";
+      if (smp.active() && de && std::string(de) != "0") {
+        if (std::string(de) == "device") {
+          TSD_CUDA(cudaStreamCreateWithPriority(&dd, cudaStreamNonBlocking, hi_pri));
+        } else {
+          dd = make_stream(0, hi_pri);
+        }
+      }
       TSD_CUDA(cudaEventCreateWithFlags(&ev_fwd0, cudaEventDisableTiming));
       TSD_CUDA(cudaEventCreateWithFlags(&ev_dedup, cudaEventDisableTiming));
     }
