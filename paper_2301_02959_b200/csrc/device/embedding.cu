@@ -442,8 +442,9 @@ template <int DIM>
 __device__ __forceinline__ float* dense_row(const DenseRange& d, uint32_t row, uint32_t** stamp) {
   const uint32_t r = row - d.lo;
   if (d.push_n) {
-    const uint32_t o = r / d.per;
-    const uint64_t slot = static_cast<uint64_t>(d.me) * d.per + (r - o * d.per);
+    const uint32_t o = d.interleave ? r % d.push_n : r / d.per;
+    const uint32_t i = d.interleave ? r / d.push_n : r - o * d.per;
+    const uint64_t slot = static_cast<uint64_t>(d.me) * d.per + i;
     *stamp = d.push_stamp[o] + slot;
     return d.push_grad[o] + slot * DIM;
   }
@@ -966,8 +967,11 @@ __global__ void __launch_bounds__(kThreads)
 replica_update_kernel(ReplicaGroup grp, OptParams opt) {
   constexpr int VEC = DIM / 32;
   const unsigned lane = threadIdx.x & 31u;
-  const uint32_t lo = grp.per * grp.me;
-  const uint32_t n = lo < grp.rows ? min(grp.per, grp.rows - lo) : 0u;  // rows I own
+  const uint32_t me = static_cast<uint32_t>(grp.me), size = static_cast<uint32_t>(grp.size);
+  const uint32_t lo = grp.per * me;
+  // rows I own: slots [0, n)
+  const uint32_t n = grp.interleave ? (grp.rows > me ? (grp.rows - me + size - 1) / size : 0u)
+                                    : (lo < grp.rows ? min(grp.per, grp.rows - lo) : 0u);
   const uint32_t gwarp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
   float* mine = grp.weights[grp.me];
@@ -989,7 +993,7 @@ replica_update_kernel(ReplicaGroup grp, OptParams opt) {
       const int b = __ffs(active) - 1;
       active &= active - 1;
       const uint32_t m = __shfl_sync(0xFFFFFFFFu, members, b);
-      const uint32_t row = lo + base + b;
+      const uint32_t row = grp.interleave ? (base + b) * size + me : lo + base + b;
       float part[kMaxGradPeers][VEC];
 #pragma unroll
       for (int k = 0; k < kMaxGradPeers; ++k) {  // touched members' partials in flight

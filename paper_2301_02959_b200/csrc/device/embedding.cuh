@@ -50,6 +50,10 @@ struct DenseRange {
   uint32_t* stamp = nullptr;
   uint32_t epoch = 0;
   uint32_t push_n = 0, per = 0, me = 0;
+  // owner of tier row r: r % push_n, its slot r / push_n (interleaved: the
+  // hot rows, first in canonical order, spread over every owner); else
+  // blocks of `per` rows, r / per
+  bool interleave = false;
   float* push_grad[kMaxGradPeers] = {};
   uint32_t* push_stamp[kMaxGradPeers] = {};
 };
@@ -151,7 +155,8 @@ void launch_dense_update(const float* grad, uint32_t rows, uint32_t row_lo, uint
 
 // Replicated-tier update over peer memory (replaces all-reduce + dense
 // update): member `me` of a replica group owns the group's rows
-// [me * per, (me + 1) * per).  Every member has already pushed its partial
+// r = i * size + me (interleave) or [me * per, (me + 1) * per); i is the
+// row's slot.  Every member has already pushed its partial
 // gradient of those rows into the owner's local receive buffer
 // recv[size][per][dim] (slot k = member k; DenseRange push mode), stamped
 // with `epoch` where it touched the row.  The owner sums the stamped
@@ -172,6 +177,7 @@ struct ReplicaGroup {
   float* state[kMaxGradPeers] = {};    // Adagrad state + row_lo (may be null)
   uint32_t rows = 0;                   // replicated rows of the tier
   uint32_t row_lo = 0;                 // local id of replicated row 0
+  bool interleave = false;             // ownership, as DenseRange::interleave
 };
 
 void launch_replica_update(const ReplicaGroup& grp, uint32_t dim, const OptParams& opt,

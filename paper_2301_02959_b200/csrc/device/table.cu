@@ -307,6 +307,9 @@ struct ts_table {
   void regrow_recv(const std::vector<uint64_t>& need);
   void exchange_recv_exports();
   uint32_t per_dp = 0, per_flex = 0;  // replicated rows owned per group member
+  // TIERSHARD_REPLICA_OWNER=block|interleave: which member owns (reduces,
+  // updates, broadcasts) replicated row r -- r / per, or r % members
+  bool replica_interleave = true;
   std::vector<float*> peer_w, peer_state;           // peers' shards (mapped)
   tsd::IpcExport my_export{};                       // staging for the step payload
   bool export_in_slot = false;                      // my_export is in our payload slot
@@ -1004,6 +1007,7 @@ void ts_table::setup_p2p() {
     TSD_CUDA(cudaEventCreateWithFlags(&ev_rep, cudaEventDisableTiming));
   }
   {
+    if (const char* oe = std::getenv("TIERSHARD_REPLICA_OWNER")) replica_interleave = std::string(oe) != "block";
     const char* re = std::getenv("TIERSHARD_ROUTE");
     route_sort = re && std::string(re) == "sort";
     const char* fe = std::getenv("TIERSHARD_FWD");
@@ -1947,6 +1951,7 @@ void ts_table::backward_p2p(const float* d_grad) {
     d0.epoch = epoch;
     d0.push_n = U;
     d0.per = per_dp;
+    d0.interleave = replica_interleave;
     d0.me = g;
     const uint64_t set = replica_deferred ? (epoch & 1u) : 0;
     for (uint32_t p = 0; p < U; ++p) {
@@ -1960,6 +1965,7 @@ void ts_table::backward_p2p(const float* d_grad) {
     d1.epoch = epoch;
     d1.push_n = N;
     d1.per = per_flex;
+    d1.interleave = replica_interleave;
     d1.me = node;
     const uint64_t set = replica_deferred ? (epoch & 1u) : 0;
     for (uint32_t k = 0; k < N; ++k) {
@@ -2096,6 +2102,7 @@ void ts_table::backward_p2p(const float* d_grad) {
     grp.recv = dense_dp.ptr + rset * dp_set_elems * cfg.dim;
     grp.recv_stamp = stamp_dp.ptr + rset * dp_set_elems;
     grp.per = per_dp;
+    grp.interleave = replica_interleave;
     grp.epoch = epoch;
     for (uint32_t p = 0; p < U; ++p) {
       grp.weights[p] = peer_w[p];
@@ -2117,6 +2124,7 @@ void ts_table::backward_p2p(const float* d_grad) {
     grp.recv = dense_flex.ptr + rset * flex_set_elems * cfg.dim;
     grp.recv_stamp = stamp_flex.ptr + rset * flex_set_elems;
     grp.per = per_flex;
+    grp.interleave = replica_interleave;
     grp.epoch = epoch;
     launch_replica_update(grp, cfg.dim, opt, rs);
   }
