@@ -526,6 +526,8 @@ def run_ours(args, dist: Dist):
     step(prof_steps)  # one more step: its timeline (both streams)
     trace = [(n, sid, round(a, 4), round(b, 4)) for n, sid, a, b in table.phase_trace()]
     all_traces = dist.gather(trace) if os.environ.get("TS_BENCH_DIAG") else None
+    rank_phases = dist.gather({k: round(v[0] / prof_steps, 4) for k, v in phases.items() if v[1]}) \
+        if os.environ.get("TS_BENCH_DIAG") else None
     table.enable_timing(False)
 
     # ---- end to end through the host-buffer public entry point -------------
@@ -790,6 +792,7 @@ def run_ours(args, dist: Dist):
         "loss_last_step": loss,
         "step_trace_ms": trace,
         **({"step_trace_ms_all_ranks": all_traces} if all_traces else {}),
+        **({"phases_ms_all_ranks": rank_phases} if rank_phases else {}),
         "wall_s_timed": round(wall, 4),
         "prep_wall_s": doc.get("prep_wall_s"),
     }

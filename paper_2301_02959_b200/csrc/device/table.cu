@@ -310,6 +310,8 @@ struct ts_table {
   // TIERSHARD_REPLICA_OWNER=block|interleave: which member owns (reduces,
   // updates, broadcasts) replicated row r -- r / per, or r % members
   bool replica_interleave = true;
+  // TIERSHARD_PUSH_ROTATE=0: the gradient push visits servers in rank order
+  bool push_rotate = true;
   std::vector<float*> peer_w, peer_state;           // peers' shards (mapped)
   tsd::IpcExport my_export{};                       // staging for the step payload
   bool export_in_slot = false;                      // my_export is in our payload slot
@@ -1008,6 +1010,7 @@ void ts_table::setup_p2p() {
   }
   {
     if (const char* oe = std::getenv("TIERSHARD_REPLICA_OWNER")) replica_interleave = std::string(oe) != "block";
+    if (const char* pr = std::getenv("TIERSHARD_PUSH_ROTATE")) push_rotate = std::string(pr) != "0";
     const char* re = std::getenv("TIERSHARD_ROUTE");
     route_sort = re && std::string(re) == "sort";
     const char* fe = std::getenv("TIERSHARD_FWD");
@@ -1992,8 +1995,11 @@ void ts_table::backward_p2p(const float* d_grad) {
       // all-gather already ordered every server's previous reads of them
       // before this step: no rendezvous, no host sync before the push
       PushTable pt{};
-      for (uint32_t p = 0; p < U; ++p) {
-        if (p == g) continue;
+      // the grid strides through the runs in table order, so every rank
+      // starts with a different server (g+1, g+2, ...): in rank order all
+      // of them would store into rank 0 first, then rank 1, ... (incast)
+      for (uint32_t i = 1; i < U; ++i) {
+        const uint32_t p = push_rotate ? (g + i) % U : (i <= g ? i - 1 : i);
         float* server_recv = peer_recv_rows[p];
         ExchangePlan sp;  // server p's receive layout: which slots hold our entries
         exchange_plan(N, W, p, h_counts.data(), &sp);
