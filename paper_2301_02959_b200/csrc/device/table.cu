@@ -533,10 +533,11 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
   use_device(c.device);
   {
     // default at U > 1 with one process per GPU (the flag-barrier peer
-    // path): the exchange streams get 48 SMs at U = 2, 56 at U >= 4, 64
-    // with several nodes, of their own.  Re-measured after the fused route
-    // and the 4-block gather (medians): 1x2 K=40 2.109, 48 2.115, 56 2.148,
-    // 64 2.242; 1x4 48 2.79, 56 2.728, 64 2.70-2.74, 72 2.856, 80 2.955.
+    // path): the exchange streams get 48 SMs at U = 2, 56 at U >= 4, of
+    // their own.  Re-measured after the fused route and the 4-block gather
+    // (medians): 1x2 K=40 2.109, 48 2.115, 56 2.148, 64 2.242; 1x4 48 2.79,
+    // 56 2.728, 64 2.70-2.74, 72 2.856, 80 2.955; after the rotated push,
+    // 2x2 3-tier 56 2.862-2.874, 64 2.939, 72 3.066.
     // Earlier, at C2 (ms/step, tools/mg_env_ab.sh): N=2 1x2
     // K=0 2.285, 40 2.231, 48 2.244, 56 2.304, 64 2.425; N=4 1x4 K=0 3.27,
     // 32 3.10, 40 2.97, 48 2.85-2.90, 64 2.95, 72 3.05; N=4 2x2 3-tier K=0
@@ -547,7 +548,7 @@ void ts_table::create(const ts_table_config& c, const uint8_t* tier_dest) {
     const char* se = std::getenv("TIERSHARD_SM_SPLIT");
     const char* xe = std::getenv("TIERSHARD_EXCHANGE");
     const bool staged = xe && std::string(xe) == "nccl";
-    const int k = se ? std::atoi(se) : ((U > 1 && !c.group && !staged) ? (N > 1 ? 64 : (U >= 4 ? 56 : 48)) : 0);
+    const int k = se ? std::atoi(se) : ((U > 1 && !c.group && !staged) ? (U >= 4 ? 56 : 48) : 0);
     if (k > 0) {
       smp = make_partition(c.device, k);
       set_sm_budget(smp.sms[1]);
