@@ -79,7 +79,7 @@ CASES = [(1, 2, 1, "p2p"), (2, 1, 1, "p2p"), (2, 1, 0, "p2p"), (2, 2, 1, "p2p"),
 # always in-process (ts_group): the C2 topologies at logical U = 8 on however
 # many GPUs the box has (several ranks per GPU), and a 2-per-GPU mix
 INPROC_CASES = [(1, 8, 1, "p2p"), (2, 4, 1, "p2p"), (2, 4, 0, "nccl"), (1, 3, 1, "p2p"), (3, 2, 1, "p2p_pull"),
-                (2, 4, 1, "p2p_fwdpull"), (2, 4, 1, "p2p_deferred")]
+                (2, 4, 1, "p2p_fwdpull"), (2, 4, 1, "p2p_deferred"), (2, 4, 1, "p2p_r1sched")]
 
 
 def case_env(exchange):
@@ -94,6 +94,8 @@ def case_env(exchange):
         env["TIERSHARD_FWD"] = "pull"
     if exchange == "p2p_deferred":
         env["TIERSHARD_REPLICA"] = "deferred"
+    if exchange == "p2p_r1sched":  # the earlier schedules: sorted route, block owners, rank-order push
+        env.update(TIERSHARD_ROUTE="sort", TIERSHARD_REPLICA_OWNER="block", TIERSHARD_PUSH_ROTATE="0")
     return env
 
 
